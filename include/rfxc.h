@@ -1,0 +1,223 @@
+/*
+ * rfxc.h — C ABI of the B200 (sm_100a) RFX proximity library (librfxc.so).
+ *
+ * The reference has no C ABI: its kernel boundary is Numba flat-array calls
+ * on caller-allocated numpy arrays.  Each entry point below
+ * replaces one of those calls (or one numpy/scipy step of the same path);
+ * the reference site is cited per function (paths relative to
+ * /root/reference/pkg/src/rfx/).
+ *
+ * Conventions
+ *   - Every pointer argument named d_* is DEVICE memory owned by the caller
+ *     (torch tensors in the Python host layer); the library never frees or
+ *     retains caller memory.  h_* pointers are host memory.
+ *   - `stream` is a cudaStream_t passed as void*; every call is
+ *     stream-ordered and asynchronous unless documented otherwise.
+ *   - Return value: RFXC_OK (0) or an error status; rfxc_last_error()
+ *     returns a thread-local message.  Python maps RFXC_EDATA -> DataError,
+ *     RFXC_EBUDGET -> BudgetError, anything else -> RfxError
+ *     (errors.py:4-19).
+ *   - Layouts: codes "nb" = (n, B) int32 row-major, exactly
+ *     LeafMembership.codes (proximity.py:73, :113-116); codes "tm" =
+ *     (B, n) int32 tree-major (device-internal).  Values are the dataset
+ *     matrix column-major (n, p), i.e. Dataset.values F-order
+ *     (dataset.py:59-71).
+ */
+#ifndef RFXC_H
+#define RFXC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    RFXC_OK = 0,
+    RFXC_EDATA = 1,    /* bad shapes / ranges        -> DataError   */
+    RFXC_EBUDGET = 2,  /* device capacity exceeded   -> BudgetError */
+    RFXC_ERUNTIME = 3, /* anything else              -> RfxError    */
+    RFXC_ECUDA = 4     /* CUDA runtime failure       -> RfxError    */
+};
+
+/* Node layouts produced by rfxc_forest_pack. */
+enum { RFXC_NODES_F32 = 0, /* 8 B/node, thresholds rounded down to f32 */
+       RFXC_NODES_F64 = 1  /* 16 B/node, f64 thresholds             */ };
+
+/* Output layouts of rfxc_pair_counts. */
+enum { RFXC_UPPER_I32 = 0,  /* packed i<j rows [row_lo,row_hi), int32 counts      */
+       RFXC_UPPER_F64 = 1,  /* packed i<j rows, count/B in f64 (FullTriangle)    */
+       RFXC_BLOCK_I32 = 2   /* (row_hi-row_lo, n) int32, j>i counted, else 0     */ };
+
+/* Quantisation modes (quantize.py:16). */
+enum { RFXC_Q_F32 = 0, RFXC_Q_F16 = 1, RFXC_Q_I8 = 2, RFXC_Q_NF4 = 3 };
+
+const char* rfxc_last_error(void);
+int rfxc_version(void);
+/* Device properties the host layer sizes grids with. */
+int rfxc_device_info(int device, int* sm_count, int64_t* l2_bytes,
+                     int64_t* smem_per_block_optin);
+
+/* ----------------------------------------------------------------- K0/K1 */
+/* Values: f64 column-major (n, p) -> f32 copy; *d_inexact set to 1 if any
+ * value is not exactly representable in f32 (then use RFXC_NODES_F64).
+ * Replaces nothing in the reference (its traversal reads f64,
+ * _kernels.py:339); it is the precondition for the exact f32 compare. */
+int rfxc_values_to_f32(const double* d_values, int64_t count, float* d_out,
+                       int32_t* d_inexact, void* stream);
+
+/* Flatten concatenated per-tree node arrays (forest.py:67-99 layout; child
+ * ids tree-local; tree b owns nodes [node_off[b], node_off[b+1])) into the
+ * packed traversal layout and compute leaf_counts (forest.py:91-93) and
+ * leaf codes (forest.py:95-99).  Requires right == left + 1 for internal
+ * nodes (trained trees satisfy it, _kernels.py:313-317; the host relays out
+ * other trees first).  d_nodes: total_nodes * (8 | 16) bytes.  d_leaf_code
+ * (nullable): explicit per-node leaf code, used for relaid-out trees whose
+ * terminal order differs from the reference node order. */
+int rfxc_forest_pack(const int8_t* d_status, const int32_t* d_split_var,
+                     const double* d_threshold, const int64_t* d_cat_mask,
+                     const int32_t* d_left, const int32_t* d_leaf_code,
+                     const int64_t* d_node_off,
+                     int32_t B, int64_t total_nodes, const uint8_t* d_col_cat,
+                     int32_t p, int32_t layout, void* d_nodes,
+                     int32_t* d_leaf_counts, void* stream);
+
+/* K1 — leaf code of every sample in trees [tree_lo, tree_hi) into
+ * d_codes_tm ((tree_hi - tree_lo) x n).  Replaces descend/descend_all
+ * (_kernels.py:333-374) driven by leaf_membership (proximity.py:100-116).
+ * d_values: f32 (layout F32) or f64 (layout F64) column-major (n, p). */
+int rfxc_leaf_codes(const void* d_nodes, const int64_t* d_node_off,
+                    int32_t layout, int32_t p, int32_t tree_lo, int32_t tree_hi,
+                    const void* d_values, int64_t n, int32_t* d_codes_tm,
+                    void* stream);
+
+/* (rows, cols) int32 transpose: tm <-> nb layouts. */
+int rfxc_transpose_i32(const int32_t* d_in, int64_t rows, int64_t cols,
+                       int32_t* d_out, void* stream);
+
+/* -------------------------------------------------------------------- K2 */
+/* Stable per-tree counting sort of samples by leaf (the bucket built inside
+ * accumulate_pair_counts[_block], _kernels.py:458-468, :491-501), done once
+ * and reused by K3/K4.  Inputs: codes_tm (Bl x n), leaf_base (Bl+1, int64,
+ * exclusive prefix of leaf_counts).  Outputs: d_perm (Bl x n): samples of
+ * tree b sorted by leaf, ascending within a leaf; d_seg (leaf_base[Bl]+1):
+ * absolute start of every leaf's run in d_perm (d_seg[last] = Bl*n).
+ * d_scratch: 4 * leaf_base[Bl] bytes. */
+int rfxc_bucket(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
+                const int64_t* d_leaf_base, int32_t max_leaf_count,
+                int32_t* d_perm, int64_t* d_seg, int32_t* d_scratch,
+                void* stream);
+
+/* -------------------------------------------------------------------- K3 */
+/* Exact same-leaf co-occurrence counts for rows [row_lo, row_hi), j > i,
+ * from codes_nb (n x B).  Replaces accumulate_pair_counts (:483-510) via
+ * _pair_counts (proximity.py:159-185) + the /B of full_proximity
+ * (proximity.py:200, IEEE f64 division) for RFXC_UPPER_F64, and
+ * accumulate_pair_counts_block (:452-480) for RFXC_BLOCK_I32.
+ * Packed layouts start at packed_index(row_lo, row_lo+1)
+ * (proximity.py:59-61) relative to d_out. */
+int rfxc_pair_counts(const int32_t* d_codes_nb, int64_t n, int32_t B,
+                     int64_t row_lo, int64_t row_hi, int32_t layout,
+                     void* d_out, void* stream);
+
+/* TriBlock tier routing (proximity.py:301-327) over packed int32 counts of
+ * rows [row_lo,row_hi): two passes.  Pass 0 writes per-row counts of
+ * hot (v >= tau) and cold (1e-6 < v < tau) entries into d_row_counts
+ * (2 * rows int64).  Pass 1 takes the exclusive row offsets (d_row_offsets,
+ * 2 * rows int64, same layout) and emits (i, j, v) sorted by (i, j). */
+int rfxc_triblock_count(const int32_t* d_counts_upper, int64_t n, int32_t B,
+                        int64_t row_lo, int64_t row_hi, double tau,
+                        int64_t* d_row_counts, void* stream);
+int rfxc_triblock_emit(const int32_t* d_counts_upper, int64_t n, int32_t B,
+                       int64_t row_lo, int64_t row_hi, double tau,
+                       const int64_t* d_row_offsets, int32_t* d_hot_i,
+                       int32_t* d_hot_j, double* d_hot_v, int32_t* d_cold_i,
+                       int32_t* d_cold_j, double* d_cold_v, void* stream);
+/* Exclusive scan of int64 (single launch, any length). */
+int rfxc_exclusive_scan_i64(const int64_t* d_in, int64_t count, int64_t* d_out,
+                            int64_t* d_total, void* stream);
+
+/* -------------------------------------------------------------------- K4 */
+/* Standard normals of PCG32 stream (seed, seq) positions [0, count) as f64
+ * (rng.py:102-115; stream jump-ahead so every thread starts mid-stream).
+ * Replaces Pcg32(seed, SEQ_FACTOR).normals((n, k)) (proximity.py:392-393)
+ * and Pcg32(seed + c, SEQ_POWER).normals(n) (mds.py:210-211). */
+int rfxc_normals(int64_t seed, int64_t seq, int64_t count, double* d_out,
+                 void* stream);
+
+/* Row-major f64 (n, k) -> f32 (n, ld) with zero padding (sketch operand). */
+int rfxc_pack_f32(const double* d_in, int64_t n, int32_t k, int32_t ld,
+                  float* d_out, void* stream);
+
+/* Leaf sums S[g, :] = sum_{i in leaf g} X[i, :] for global leaves
+ * [g_lo, g_hi) (one phase of Mt @ X, proximity.py:394).  X: f32 (n, ld);
+ * S: f32 ((g_hi - g_lo), ld). */
+int rfxc_leaf_sums(const int32_t* d_perm, const int64_t* d_seg, int64_t g_lo,
+                   int64_t g_hi, const float* d_X, int32_t k, int32_t ld,
+                   float* d_S, void* stream);
+
+/* Gather Y[i, :] (+)= scale * sum_b S[leaf_base[b] + codes_nb[i, b], :]
+ * over the Bl local trees (the M @ (.) phase, proximity.py:394).
+ * Y: f64 (n, k).  accumulate != 0 adds into Y. */
+int rfxc_leaf_gather(const int32_t* d_codes_nb, int64_t n, int32_t Bl,
+                     const int64_t* d_leaf_base, const float* d_S, int32_t k,
+                     int32_t ld, double scale, int32_t accumulate, double* d_Y,
+                     void* stream);
+
+/* -------------------------------------------------------------------- K5 */
+/* C = A^T B for row-major f64 A (n, ka), B (n, kb): deterministic two-level
+ * reduction (Gram of the QR steps, proximity.py:395-398, and
+ * T = Q^T (P Q)).  d_partials: nparts * ka * kb f64, nparts from
+ * rfxc_gram_parts().  Result C (ka x kb) row-major f64 on device. */
+int rfxc_gram_parts(int64_t n);
+int rfxc_gram(const double* d_A, const double* d_B, int64_t n, int32_t ka,
+              int32_t kb, double* d_partials, double* d_C, void* stream);
+
+/* Y (n, ka) times small M (ka, kb) -> Z (n, kb) f64; optional f32 copy
+ * (n, ld32) for the next sketch pass (d_Z32 may be NULL). */
+int rfxc_matmul_small(const double* d_Y, int64_t n, int32_t ka,
+                      const double* d_M, int32_t kb, double* d_Z,
+                      float* d_Z32, int32_t ld32, void* stream);
+
+/* -------------------------------------------------------------------- K6 */
+/* factor = Q (n, k) @ Wr (k, r) followed by quantisation (quantize.py:83-117,
+ * i8: per-column absmax/127, rint half-even, clip +-127).
+ * d_factor: f64 (n, r) scratch/output; d_colmax_parts: rfxc_gram_parts(n)*r
+ * f64; d_scales: r f64 (i8) / nblocks (nf4); d_data: mode-dependent output
+ * (i8: int8 (n, r); f32; f16; nf4: packed uint8, column-major 64-blocks). */
+int rfxc_factor_quantize(const double* d_Q, int64_t n, int32_t k,
+                         const double* d_Wr, int32_t r, int32_t mode,
+                         double* d_factor, double* d_colmax_parts,
+                         double* d_scales, void* d_data, void* stream);
+
+/* -------------------------------------------------------------------- K7 */
+/* pmax (proximity.py:406-417): max over diag(dq dq^T) and 1024 sampled
+ * off-diagonal pairs drawn on device from Pcg32(seed, SEQ_PMAX).
+ * d_dq: dequantised factor f64 (n, r).  d_out: 1 f64. d_parts: scratch of
+ * rfxc_gram_parts(n) f64. */
+int rfxc_dequantize(const void* d_data, const double* d_scales, int64_t n,
+                    int32_t r, int32_t mode, double* d_dq, void* stream);
+int rfxc_pmax(const double* d_dq, int64_t n, int32_t r, int64_t seed,
+              double* d_parts, double* d_out, void* stream);
+
+/* ----------------------------------------------------------------- K8/K9 */
+/* Factor-space MDS power iteration (mds.py:184-268) as one persistent
+ * cooperative kernel: k eigenpairs, implicit deflation, Rayleigh quotient,
+ * tol on max|v_new - v|, iteration cap, stop at lambda <= 0.  The Gram
+ * matvec is gram_matvec (mds.py:161-181) on the UNclamped P = dq dq^T.
+ * Outputs: d_coords (n, k) row-major f64 = sqrt(lambda) * sign_fixed v
+ * (mds.py:257-261); d_info: per component {lambda, iterations, residual,
+ * converged} as 4 f64; *d_k_used (int32).  d_work: rfxc_mds_work_bytes(). */
+int64_t rfxc_mds_work_bytes(int64_t n, int32_t r, int32_t k);
+int rfxc_mds_power(const double* d_dq, int64_t n, int32_t r, double pmax,
+                   int32_t k, int32_t max_iterations, double tol, int64_t seed,
+                   double* d_coords, double* d_info, int32_t* d_k_used,
+                   void* d_work, void* stream);
+/* One gram_matvec (mds.py:161-181): d_w = G v. */
+int rfxc_gram_matvec(const double* d_dq, int64_t n, int32_t r, double pmax,
+                     const double* d_v, double* d_w, void* d_work,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RFXC_H */

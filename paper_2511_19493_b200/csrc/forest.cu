@@ -1,0 +1,333 @@
+// forest.cu — K0 (forest flattening) and K1 (forest traversal to leaf codes).
+//
+// Reference: descend / descend_all (_kernels.py:333-374) driven per tree by
+// leaf_membership (proximity.py:100-116), leaf ordinals from
+// Tree.leaf_codes (forest.py:95-99).
+//
+// Design (B200): a CTA owns a tile of T samples and walks them down a chunk
+// of trees.  The tile's feature rows are staged once into shared memory with
+// coalesced column loads (Dataset.values is column-major), so every
+// per-level feature read is a shared-memory access; node records (8 B in the
+// f32 layout) are read through the read-only L1 path, where the upper levels
+// of the tree currently being walked by every warp of the SM stay resident.
+// Each thread advances ILP independent root-to-leaf chains (one per tree) so
+// dependent node loads overlap.  Codes are written tree-major, coalesced.
+//
+// Exactness of the f32 layout: thresholds are rounded toward -inf to f32.
+// For any f32-representable x, x <= t (f64)  <=>  x <= RD_f32(t), so the
+// comparison is bit-exact with the reference whenever every value is
+// f32-exact (checked by rfxc_values_to_f32; otherwise the f64 layout runs).
+#include "common.cuh"
+
+namespace rfxc {
+
+// ---------------------------------------------------------------- K0 pack
+__global__ void values_to_f32_kernel(const double* __restrict__ in, int64_t count,
+                                     float* __restrict__ out, int32_t* inexact)
+{
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double x = in[i];
+        float f = (float)x;
+        out[i] = f;
+        bad |= ((double)f != x);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(inexact, 1);
+}
+
+__host__ __device__ inline int feature_bits(int p)
+{
+    int fb = 1;
+    while ((1 << fb) < p) fb++;
+    return fb;
+}
+
+// One CTA per tree: block-wide exclusive scan of the terminal flags gives the
+// dense leaf ordinal of every terminal (forest.py:95-99).
+template <int LAYOUT>
+__global__ void pack_kernel(const int8_t* __restrict__ status,
+                            const int32_t* __restrict__ split_var,
+                            const double* __restrict__ threshold,
+                            const int64_t* __restrict__ cat_mask,
+                            const int32_t* __restrict__ left,
+                            const int32_t* __restrict__ leaf_code,
+                            const int64_t* __restrict__ node_off,
+                            const uint8_t* __restrict__ col_cat, int fb,
+                            void* nodes_out, int32_t* leaf_counts)
+{
+    __shared__ int warp_tot[32];
+    __shared__ int carry;
+    const int b = blockIdx.x;
+    const int64_t o = node_off[b], nc = node_off[b + 1] - o;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < nc; base += blockDim.x) {
+        int64_t t = base + threadIdx.x;
+        int is_leaf = (t < nc) ? (status[o + t] == 1) : 0;
+        unsigned ball = __ballot_sync(0xffffffffu, is_leaf);
+        int within = __popc(ball & ((1u << lane) - 1u));
+        if (lane == 0) warp_tot[warp] = __popc(ball);
+        __syncthreads();
+        int before = carry;
+        for (int w = 0; w < warp; w++) before += warp_tot[w];
+        if (t < nc) {
+            int64_t g = o + t;
+            if (LAYOUT == RFXC_NODES_F32) {
+                uint2 rec;
+                if (is_leaf) {
+                    rec.x = (uint32_t)(leaf_code ? leaf_code[g] : before + within);
+                    rec.y = 0u;
+                } else {
+                    int f = split_var[g];
+                    uint32_t cat = col_cat[f] == 1;
+                    rec.x = cat ? (uint32_t)(cat_mask[g] & 0xffffffffLL)
+                                : __float_as_uint(__double2float_rd(threshold[g]));
+                    rec.y = ((uint32_t)left[g] << (fb + 1)) | (cat << fb) | (uint32_t)f;
+                }
+                reinterpret_cast<uint2*>(nodes_out)[g] = rec;
+            } else {
+                int4 rec;
+                if (is_leaf) {
+                    rec = make_int4(0, 0, -1, leaf_code ? leaf_code[g] : before + within);
+                } else {
+                    int f = split_var[g];
+                    int cat = col_cat[f] == 1;
+                    long long bits = cat ? (long long)cat_mask[g]
+                                         : __double_as_longlong(threshold[g]);
+                    rec = make_int4((int)(bits & 0xffffffffLL), (int)(bits >> 32),
+                                    f | (cat << 30), left[g]);
+                }
+                reinterpret_cast<int4*>(nodes_out)[g] = rec;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int s = 0;
+            for (int w = 0; w < nw; w++) s += warp_tot[w];
+            carry += s;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) leaf_counts[b] = carry;
+}
+
+// ------------------------------------------------------------ K1 traverse
+constexpr int TRAV_T = 128;   // samples per CTA (one per thread)
+constexpr int TRAV_ILP = 4;   // independent tree chains per thread
+
+template <int LAYOUT, bool SMEM_X>
+__global__ void __launch_bounds__(TRAV_T)
+traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ node_off,
+                int fb, int p, int tree_lo, int tree_hi, int trees_per_chunk,
+                const void* __restrict__ values_v, int64_t n,
+                int32_t* __restrict__ codes_tm)
+{
+    using V = typename std::conditional<LAYOUT == RFXC_NODES_F32, float, double>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* xs = reinterpret_cast<V*>(smem_raw);
+    const V* __restrict__ X = reinterpret_cast<const V*>(values_v);
+    const int t = threadIdx.x;
+    const int64_t i0 = (int64_t)blockIdx.x * TRAV_T;
+    const int64_t i = i0 + t;
+    const bool valid = i < n;
+    const int stride = p + 1;  // odd row stride spreads banks
+    if (SMEM_X) {
+        // coalesced: consecutive threads read consecutive samples of feature f
+        for (int f = 0; f < p; f++) {
+            V v = valid ? X[(int64_t)f * n + i] : V(0);
+            xs[t * stride + f] = v;
+        }
+        __syncthreads();
+    }
+    const int b_begin = tree_lo + blockIdx.y * trees_per_chunk;
+    const int b_end = min(tree_hi, b_begin + trees_per_chunk);
+    if (!valid) return;
+    const uint32_t fmask = (1u << fb) - 1u;
+
+    for (int b = b_begin; b < b_end; b += TRAV_ILP) {
+        int64_t base[TRAV_ILP];
+        uint32_t id[TRAV_ILP];
+        int32_t code[TRAV_ILP];
+        bool act[TRAV_ILP];
+#pragma unroll
+        for (int c = 0; c < TRAV_ILP; c++) {
+            act[c] = (b + c) < b_end;
+            base[c] = act[c] ? node_off[b + c] : 0;
+            id[c] = 0;
+            code[c] = 0;
+        }
+        bool any = true;
+        while (any) {
+            any = false;
+#pragma unroll
+            for (int c = 0; c < TRAV_ILP; c++) {
+                if (!act[c]) continue;
+                if (LAYOUT == RFXC_NODES_F32) {
+                    uint2 nd = __ldg(reinterpret_cast<const uint2*>(nodes_v) + base[c] + id[c]);
+                    if (nd.y == 0u) {
+                        code[c] = (int32_t)nd.x;
+                        act[c] = false;
+                        continue;
+                    }
+                    const uint32_t f = nd.y & fmask;
+                    const float v = SMEM_X ? (float)xs[t * stride + f]
+                                           : (float)X[(int64_t)f * n + i];
+                    bool go;
+                    if ((nd.y >> fb) & 1u) {
+                        uint32_t lv = (uint32_t)(int)v;
+                        go = lv < 32u ? ((nd.x >> lv) & 1u) : false;
+                    } else {
+                        go = v <= __uint_as_float(nd.x);
+                    }
+                    id[c] = (nd.y >> (fb + 1)) + (go ? 0u : 1u);
+                } else {
+                    int4 nd = __ldg(reinterpret_cast<const int4*>(nodes_v) + base[c] + id[c]);
+                    if (nd.z < 0) {
+                        code[c] = nd.w;
+                        act[c] = false;
+                        continue;
+                    }
+                    const int f = nd.z & 0x3fffffff;
+                    const double v = SMEM_X ? (double)xs[t * stride + f]
+                                            : (double)X[(int64_t)f * n + i];
+                    long long bits = ((long long)(unsigned)nd.y << 32) | (unsigned)nd.x;
+                    bool go;
+                    if (nd.z & (1 << 30)) {
+                        long long lv = (long long)v;
+                        go = (lv >= 0 && lv < 64) ? ((bits >> lv) & 1LL) : false;
+                    } else {
+                        go = v <= __longlong_as_double(bits);
+                    }
+                    id[c] = (uint32_t)nd.w + (go ? 0u : 1u);
+                }
+                any = true;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < TRAV_ILP; c++)
+            if ((b + c) < b_end) codes_tm[(int64_t)(b + c - tree_lo) * n + i] = code[c];
+    }
+}
+
+__global__ void transpose_i32_kernel(const int32_t* __restrict__ in, int64_t rows,
+                                     int64_t cols, int32_t* __restrict__ out)
+{
+    __shared__ int32_t tile[32][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        int64_t r = r0 + k, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        int64_t c = c0 + k, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+    }
+}
+
+}  // namespace rfxc
+
+using namespace rfxc;
+
+extern "C" int rfxc_values_to_f32(const double* d_values, int64_t count, float* d_out,
+                                  int32_t* d_inexact, void* stream)
+{
+    if (count < 0) return fail(RFXC_EDATA, "values_to_f32: negative count");
+    if (count == 0) return RFXC_OK;
+    int grid = (int)std::min<int64_t>(ceil_div(count, 256), (int64_t)sm_count() * 8);
+    values_to_f32_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_values, count, d_out, d_inexact);
+    return check_launch("values_to_f32");
+}
+
+extern "C" int rfxc_forest_pack(const int8_t* d_status, const int32_t* d_split_var,
+                                const double* d_threshold, const int64_t* d_cat_mask,
+                                const int32_t* d_left, const int32_t* d_leaf_code,
+                                const int64_t* d_node_off, int32_t B,
+                                int64_t total_nodes, const uint8_t* d_col_cat, int32_t p,
+                                int32_t layout, void* d_nodes, int32_t* d_leaf_counts,
+                                void* stream)
+{
+    if (B < 1 || p < 1 || total_nodes < B) return fail(RFXC_EDATA, "forest_pack: bad shape");
+    const int fb = feature_bits(p);
+    if (layout == RFXC_NODES_F32) {
+        pack_kernel<RFXC_NODES_F32><<<B, 256, 0, as_stream(stream)>>>(
+            d_status, d_split_var, d_threshold, d_cat_mask, d_left, d_leaf_code, d_node_off, d_col_cat, fb,
+            d_nodes, d_leaf_counts);
+    } else if (layout == RFXC_NODES_F64) {
+        pack_kernel<RFXC_NODES_F64><<<B, 256, 0, as_stream(stream)>>>(
+            d_status, d_split_var, d_threshold, d_cat_mask, d_left, d_leaf_code, d_node_off, d_col_cat, fb,
+            d_nodes, d_leaf_counts);
+    } else {
+        return fail(RFXC_EDATA, "forest_pack: unknown layout %d", layout);
+    }
+    return check_launch("forest_pack");
+}
+
+template <int LAYOUT, bool SMEM_X>
+static int launch_traverse(const void* d_nodes, const int64_t* d_node_off, int p, int tree_lo,
+                           int tree_hi, const void* d_values, int64_t n, int32_t* d_codes_tm,
+                           size_t smem, cudaStream_t st)
+{
+    auto kern = traverse_kernel<LAYOUT, SMEM_X>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return fail(RFXC_ECUDA, "traverse attr: %s", cudaGetErrorString(e));
+    }
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TRAV_T, smem);
+    occ = std::max(occ, 1);
+    const int64_t tiles = ceil_div(n, TRAV_T);
+    const int nt = tree_hi - tree_lo;
+    // enough CTAs for ~6 waves; every chunk a multiple of the chain count
+    int64_t want = (int64_t)sm_count() * occ * 6;
+    int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(want, tiles), nt));
+    int per = (int)ceil_div(nt, chunks);
+    per = (int)ceil_div(per, TRAV_ILP) * TRAV_ILP;
+    chunks = (int)ceil_div(nt, per);
+    dim3 grid((unsigned)tiles, (unsigned)chunks);
+    kern<<<grid, TRAV_T, smem, st>>>(d_nodes, d_node_off, feature_bits(p), p, tree_lo, tree_hi,
+                                     per, d_values, n, d_codes_tm);
+    return check_launch("leaf_codes");
+}
+
+extern "C" int rfxc_leaf_codes(const void* d_nodes, const int64_t* d_node_off, int32_t layout,
+                               int32_t p, int32_t tree_lo, int32_t tree_hi,
+                               const void* d_values, int64_t n, int32_t* d_codes_tm,
+                               void* stream)
+{
+    if (n < 1 || p < 1 || tree_lo < 0 || tree_hi <= tree_lo)
+        return fail(RFXC_EDATA, "leaf_codes: bad shape");
+    cudaStream_t st = as_stream(stream);
+    const size_t vsz = layout == RFXC_NODES_F32 ? 4 : 8;
+    const size_t smem = (size_t)TRAV_T * (p + 1) * vsz;
+    const bool use_smem = smem <= 112 * 1024;
+    if (layout == RFXC_NODES_F32)
+        return use_smem ? launch_traverse<RFXC_NODES_F32, true>(d_nodes, d_node_off, p, tree_lo,
+                                                                tree_hi, d_values, n, d_codes_tm,
+                                                                smem, st)
+                        : launch_traverse<RFXC_NODES_F32, false>(d_nodes, d_node_off, p, tree_lo,
+                                                                 tree_hi, d_values, n,
+                                                                 d_codes_tm, 0, st);
+    if (layout == RFXC_NODES_F64)
+        return use_smem ? launch_traverse<RFXC_NODES_F64, true>(d_nodes, d_node_off, p, tree_lo,
+                                                                tree_hi, d_values, n, d_codes_tm,
+                                                                smem, st)
+                        : launch_traverse<RFXC_NODES_F64, false>(d_nodes, d_node_off, p, tree_lo,
+                                                                 tree_hi, d_values, n,
+                                                                 d_codes_tm, 0, st);
+    return fail(RFXC_EDATA, "leaf_codes: unknown layout %d", layout);
+}
+
+extern "C" int rfxc_transpose_i32(const int32_t* d_in, int64_t rows, int64_t cols,
+                                  int32_t* d_out, void* stream)
+{
+    if (rows < 0 || cols < 0) return fail(RFXC_EDATA, "transpose: bad shape");
+    if (rows == 0 || cols == 0) return RFXC_OK;
+    dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+    transpose_i32_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(d_in, rows, cols, d_out);
+    return check_launch("transpose_i32");
+}

@@ -1,0 +1,284 @@
+// pairs.cu — K3: exact same-leaf co-occurrence counts + TriBlock routing.
+//
+// Reference: accumulate_pair_counts (_kernels.py:483-510) orchestrated by
+// _pair_counts (proximity.py:159-185), the /B of full_proximity
+// (proximity.py:199-200), accumulate_pair_counts_block (_kernels.py:452-480)
+// and the tier routing of triblock_proximity (proximity.py:301-327).
+//
+// Round-1 design: output-stationary 128x128 tiles of the upper triangle.
+// Each CTA stages 32-tree slices of its row block's and column block's
+// codes (read coalesced from the (n, B) membership) into shared memory and
+// every thread accumulates an 8x8 register micro-tile of int32 counts with
+// integer compares.  The count for (i, j) is sum_b [code_b(i) == code_b(j)],
+// the same integer the reference accumulates one increment at a time, so the
+// output is bit-exact by construction and independent of leaf sizes.  The
+// epilogue fuses the layout: packed int32, packed f64 count/B (an IEEE
+// division, bit-identical to counts / float(B)), or the TriBlock row block.
+#include "common.cuh"
+
+namespace rfxc {
+
+constexpr int PT = 128;     // tile edge
+constexpr int PK = 32;      // trees per smem slice
+constexpr int PTHREADS = 256;
+
+__device__ __forceinline__ int64_t row_start(int64_t i, int64_t n)
+{
+    return i * (2 * n - i - 1) / 2;  // packed index of (i, i+1)
+}
+
+template <int LAYOUT>
+__global__ void __launch_bounds__(PTHREADS)
+pair_tile_kernel(const int32_t* __restrict__ codes, int64_t n, int32_t B, int64_t row_lo,
+                 int64_t row_hi, void* __restrict__ out)
+{
+    const int64_t R = blockIdx.y, C = blockIdx.x;
+    if (C < R) return;  // strictly below the diagonal band: j < i everywhere
+    const int64_t i0 = row_lo + R * PT, j0 = row_lo + C * PT;
+    if (i0 >= row_hi || j0 >= n) return;
+
+    __shared__ __align__(16) int32_t As[PK][PT];
+    __shared__ __align__(16) int32_t Bs[PK][PT];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    int acc[8][8];
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int c = 0; c < 8; c++) acc[a][c] = 0;
+
+    for (int b0 = 0; b0 < B; b0 += PK) {
+        const int kk = min(PK, B - b0);
+        // coalesced along trees: lane -> tree, row loop across threads
+        for (int e = tid; e < PT * PK; e += PTHREADS) {
+            const int r = e / PK, k = e % PK;
+            int32_t va = -1, vb = -2;  // distinct sentinels never compare equal
+            if (k < kk) {
+                const int64_t i = i0 + r, j = j0 + r;
+                if (i < row_hi) va = __ldg(codes + i * B + b0 + k);
+                if (j < n) vb = __ldg(codes + j * B + b0 + k);
+            }
+            As[k][r] = va;
+            Bs[k][r] = vb;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int k = 0; k < kk; k++) {
+            const int4 a0 = *reinterpret_cast<const int4*>(&As[k][ty * 8]);
+            const int4 a1 = *reinterpret_cast<const int4*>(&As[k][ty * 8 + 4]);
+            const int4 c0 = *reinterpret_cast<const int4*>(&Bs[k][tx * 8]);
+            const int4 c1 = *reinterpret_cast<const int4*>(&Bs[k][tx * 8 + 4]);
+            const int ra[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const int rc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+            for (int a = 0; a < 8; a++)
+#pragma unroll
+                for (int c = 0; c < 8; c++) acc[a][c] += (ra[a] == rc[c]);
+        }
+        __syncthreads();
+    }
+
+    // epilogue: (i, j) with j > i only
+#pragma unroll
+    for (int a = 0; a < 8; a++) {
+        const int64_t i = i0 + ty * 8 + a;
+        if (i >= row_hi) continue;
+        const int64_t rbase = row_start(i, n) - row_start(row_lo, n) - i - 1;
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const int64_t j = j0 + tx * 8 + c;
+            if (j <= i || j >= n) continue;
+            if (LAYOUT == RFXC_UPPER_I32)
+                reinterpret_cast<int32_t*>(out)[rbase + j] = acc[a][c];
+            else if (LAYOUT == RFXC_UPPER_F64)
+                reinterpret_cast<double*>(out)[rbase + j] = (double)acc[a][c] / (double)B;
+            else
+                reinterpret_cast<int32_t*>(out)[(i - row_lo) * n + j] = acc[a][c];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- TriBlock
+constexpr double ZERO_TIER = 1e-6;  // proximity.py:39
+
+__global__ void triblock_count_kernel(const int32_t* __restrict__ counts, int64_t n, int32_t B,
+                                      int64_t row_lo, int64_t row_hi, double tau,
+                                      int64_t* __restrict__ row_counts)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = row_hi - row_lo;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double dB = (double)B;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        const int64_t i = row_lo + r;
+        const int32_t* row = counts + (row_start(i, n) - row_start(row_lo, n));
+        const int64_t m = n - i - 1;
+        int hot = 0, cold = 0;
+        for (int64_t q = lane; q < m; q += 32) {
+            const double v = (double)row[q] / dB;
+            if (v > ZERO_TIER) {
+                if (v >= tau) hot++;
+                else cold++;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            hot += __shfl_xor_sync(0xffffffffu, hot, o);
+            cold += __shfl_xor_sync(0xffffffffu, cold, o);
+        }
+        if (lane == 0) {
+            row_counts[r] = hot;
+            row_counts[rows + r] = cold;
+        }
+    }
+}
+
+__global__ void triblock_emit_kernel(const int32_t* __restrict__ counts, int64_t n, int32_t B,
+                                     int64_t row_lo, int64_t row_hi, double tau,
+                                     const int64_t* __restrict__ row_off, int32_t* hot_i,
+                                     int32_t* hot_j, double* hot_v, int32_t* cold_i,
+                                     int32_t* cold_j, double* cold_v)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t rows = row_hi - row_lo;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double dB = (double)B;
+    for (int64_t r = warp; r < rows; r += nwarps) {
+        const int64_t i = row_lo + r;
+        const int32_t* row = counts + (row_start(i, n) - row_start(row_lo, n));
+        const int64_t m = n - i - 1;
+        int64_t ph = row_off[r], pc = row_off[rows + r];
+        for (int64_t q0 = 0; q0 < m; q0 += 32) {
+            const int64_t q = q0 + lane;
+            double v = 0.0;
+            if (q < m) v = (double)row[q] / dB;
+            const bool keep = v > ZERO_TIER;
+            const bool is_hot = keep && v >= tau, is_cold = keep && !(v >= tau);
+            const unsigned mh = __ballot_sync(0xffffffffu, is_hot);
+            const unsigned mc = __ballot_sync(0xffffffffu, is_cold);
+            const int32_t j = (int32_t)(i + 1 + q);
+            if (is_hot) {
+                const int64_t at = ph + __popc(mh & lt);
+                hot_i[at] = (int32_t)i;
+                hot_j[at] = j;
+                hot_v[at] = v;
+            }
+            if (is_cold) {
+                const int64_t at = pc + __popc(mc & lt);
+                cold_i[at] = (int32_t)i;
+                cold_j[at] = j;
+                cold_v[at] = v;
+            }
+            ph += __popc(mh);
+            pc += __popc(mc);
+        }
+    }
+}
+
+// Single-CTA exclusive scan (int64), chunked with a running carry.
+__global__ void __launch_bounds__(1024)
+scan_i64_kernel(const int64_t* __restrict__ in, int64_t count, int64_t* __restrict__ out,
+                int64_t* total)
+{
+    __shared__ int64_t wsum[32];
+    __shared__ int64_t carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < count; base += 1024) {
+        const int64_t idx = base + tid;
+        const int64_t v = idx < count ? in[idx] : 0;
+        int64_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        int64_t before = carry;
+        for (int w = 0; w < warp; w++) before += wsum[w];
+        if (idx < count) out[idx] = before + incl - v;
+        __syncthreads();
+        if (tid == 0) {
+            int64_t s = 0;
+            for (int w = 0; w < 32; w++) s += wsum[w];
+            carry += s;
+        }
+        __syncthreads();
+    }
+    if (tid == 0 && total) *total = carry;
+}
+
+}  // namespace rfxc
+
+using namespace rfxc;
+
+extern "C" int rfxc_pair_counts(const int32_t* d_codes_nb, int64_t n, int32_t B, int64_t row_lo,
+                                int64_t row_hi, int32_t layout, void* d_out, void* stream)
+{
+    if (n < 2 || B < 1 || row_lo < 0 || row_hi > n || row_lo >= row_hi)
+        return fail(RFXC_EDATA, "pair_counts: bad shape n=%lld rows=[%lld,%lld)", (long long)n,
+                    (long long)row_lo, (long long)row_hi);
+    cudaStream_t st = as_stream(stream);
+    const int64_t rb = ceil_div(row_hi - row_lo, PT), cb = ceil_div(n - row_lo, PT);
+    if (rb > 65535) return fail(RFXC_EDATA, "pair_counts: too many row blocks; shard rows");
+    dim3 grid((unsigned)cb, (unsigned)rb);
+    switch (layout) {
+    case RFXC_UPPER_I32:
+        pair_tile_kernel<RFXC_UPPER_I32><<<grid, PTHREADS, 0, st>>>(d_codes_nb, n, B, row_lo,
+                                                                    row_hi, d_out);
+        break;
+    case RFXC_UPPER_F64:
+        pair_tile_kernel<RFXC_UPPER_F64><<<grid, PTHREADS, 0, st>>>(d_codes_nb, n, B, row_lo,
+                                                                    row_hi, d_out);
+        break;
+    case RFXC_BLOCK_I32: {
+        cudaError_t e = cudaMemsetAsync(d_out, 0, (size_t)(row_hi - row_lo) * n * 4, st);
+        if (e != cudaSuccess) return fail(RFXC_ECUDA, "memset: %s", cudaGetErrorString(e));
+        pair_tile_kernel<RFXC_BLOCK_I32><<<grid, PTHREADS, 0, st>>>(d_codes_nb, n, B, row_lo,
+                                                                    row_hi, d_out);
+        break;
+    }
+    default:
+        return fail(RFXC_EDATA, "pair_counts: unknown layout %d", layout);
+    }
+    return check_launch("pair_counts");
+}
+
+extern "C" int rfxc_triblock_count(const int32_t* d_counts_upper, int64_t n, int32_t B,
+                                   int64_t row_lo, int64_t row_hi, double tau,
+                                   int64_t* d_row_counts, void* stream)
+{
+    if (row_lo < 0 || row_hi > n || row_lo >= row_hi) return fail(RFXC_EDATA, "triblock: rows");
+    int64_t rows = row_hi - row_lo;
+    int grid = (int)std::min<int64_t>(ceil_div(rows * 32, 256), (int64_t)sm_count() * 16);
+    triblock_count_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_counts_upper, n, B, row_lo,
+                                                               row_hi, tau, d_row_counts);
+    return check_launch("triblock_count");
+}
+
+extern "C" int rfxc_triblock_emit(const int32_t* d_counts_upper, int64_t n, int32_t B,
+                                  int64_t row_lo, int64_t row_hi, double tau,
+                                  const int64_t* d_row_offsets, int32_t* d_hot_i, int32_t* d_hot_j,
+                                  double* d_hot_v, int32_t* d_cold_i, int32_t* d_cold_j,
+                                  double* d_cold_v, void* stream)
+{
+    if (row_lo < 0 || row_hi > n || row_lo >= row_hi) return fail(RFXC_EDATA, "triblock: rows");
+    int64_t rows = row_hi - row_lo;
+    int grid = (int)std::min<int64_t>(ceil_div(rows * 32, 256), (int64_t)sm_count() * 16);
+    triblock_emit_kernel<<<grid, 256, 0, as_stream(stream)>>>(
+        d_counts_upper, n, B, row_lo, row_hi, tau, d_row_offsets, d_hot_i, d_hot_j, d_hot_v,
+        d_cold_i, d_cold_j, d_cold_v);
+    return check_launch("triblock_emit");
+}
+
+extern "C" int rfxc_exclusive_scan_i64(const int64_t* d_in, int64_t count, int64_t* d_out,
+                                       int64_t* d_total, void* stream)
+{
+    if (count < 0) return fail(RFXC_EDATA, "scan: negative count");
+    scan_i64_kernel<<<1, 1024, 0, as_stream(stream)>>>(d_in, count, d_out, d_total);
+    return check_launch("exclusive_scan_i64");
+}

@@ -1,0 +1,260 @@
+// quant.cu — K6/K7: factor = Q Wr, QLORA quantisation, dequantisation, pmax.
+//
+// Reference: proximity.py:401-417 (factor_raw = Q @ (W_r * sqrt(lambda)),
+// quantize, dequantize, pmax over the diagonal and 1024 sampled pairs) and
+// quantize.py:83-140 (f32 / f16 casts, i8 per-column absmax/127 with
+// round-half-even and clip to +-127, nf4 64-blocks of the column-major
+// flatten against the 16-level codebook, low nibble first).
+//
+// Every division is a true IEEE f64 division and rint() is round-half-even,
+// so for the same factor the device codes equal numpy's bit for bit.
+#include <cuda_fp16.h>
+
+#include "../csrc/host/pcg32.h"
+#include "common.cuh"
+
+namespace rfxc {
+
+__constant__ double NF4_CB[16] = {
+    -1.0, -0.6961928009986877, -0.5250730514526367, -0.39491748809814453,
+    -0.28444138169288635, -0.18477343022823334, -0.09105003625154495, 0.0,
+    0.07958029955625534, 0.16093020141124725, 0.24611230194568634, 0.33791524171829224,
+    0.44070982933044434, 0.5626170039176941, 0.7229568362236023, 1.0};
+
+int gram_parts(int64_t n);
+
+// F = Q @ Wr row by row; per-part column absmax.
+__global__ void __launch_bounds__(256)
+factor_kernel(const double* __restrict__ Q, int64_t n, int k, const double* __restrict__ Wr, int r,
+              int64_t rows_per_part, double* __restrict__ F, double* __restrict__ colmax_parts)
+{
+    extern __shared__ double wsm[];  // k x r
+    double* cm = wsm + k * r;        // blockDim partial maxima per column slot
+    for (int e = threadIdx.x; e < k * r; e += blockDim.x) wsm[e] = Wr[e];
+    __syncthreads();
+    const int64_t r0 = blockIdx.x * rows_per_part, r1 = min(n, r0 + rows_per_part);
+    // thread -> (row offset, column): columns fastest
+    const int c = threadIdx.x % r;
+    const int rstep = blockDim.x / r;
+    const int roff = threadIdx.x / r;
+    double m = 0.0;
+    if (roff < rstep) {
+        for (int64_t i = r0 + roff; i < r1; i += rstep) {
+            double s = 0.0;
+            for (int a = 0; a < k; a++) s += Q[i * k + a] * wsm[a * r + c];
+            F[i * r + c] = s;
+            m = fmax(m, fabs(s));
+        }
+    }
+    cm[threadIdx.x] = (roff < rstep) ? m : 0.0;
+    __syncthreads();
+    if (threadIdx.x < r) {
+        double mm = 0.0;
+        for (int q = 0; q < rstep; q++) mm = fmax(mm, cm[q * r + threadIdx.x]);
+        colmax_parts[(int64_t)blockIdx.x * r + threadIdx.x] = mm;
+    }
+}
+
+__global__ void colmax_final_kernel(const double* __restrict__ parts, int nparts, int r,
+                                     double* __restrict__ scales)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= r) return;
+    double m = 0.0;
+    for (int q = 0; q < nparts; q++) m = fmax(m, parts[(int64_t)q * r + c]);
+    scales[c] = m / 127.0;  // quantize.py:95-96
+}
+
+__global__ void quant_i8_kernel(const double* __restrict__ F, int64_t total, int r,
+                                const double* __restrict__ scales, int8_t* __restrict__ out)
+{
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const double s = scales[e % r];
+        const double safe = s > 0.0 ? s : 1.0;
+        double q = rint(F[e] / safe);
+        q = fmin(127.0, fmax(-127.0, q));
+        out[e] = (int8_t)q;
+    }
+}
+
+__global__ void quant_cast_kernel(const double* __restrict__ F, int64_t total, int mode,
+                                  void* __restrict__ out)
+{
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (mode == RFXC_Q_F32) reinterpret_cast<float*>(out)[e] = (float)F[e];
+        else reinterpret_cast<__half*>(out)[e] = __double2half(F[e]);
+    }
+}
+
+// nf4: flat index f = c*n + i (column-major), block = f / 64.
+__global__ void quant_nf4_kernel(const double* __restrict__ F, int64_t n, int r, int64_t nblocks,
+                                 double* __restrict__ absmax, uint8_t* __restrict__ out)
+{
+    const int64_t blk = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (blk >= nblocks) return;
+    const int64_t total = n * r;
+    double m = 0.0;
+    for (int q = 0; q < 64; q++) {
+        const int64_t f = blk * 64 + q;
+        if (f < total) m = fmax(m, fabs(F[(f % n) * r + f / n]));
+    }
+    absmax[blk] = m;
+    const double safe = m > 0.0 ? m : 1.0;
+    for (int q = 0; q < 64; q += 2) {
+        uint8_t code[2];
+        for (int h = 0; h < 2; h++) {
+            const int64_t f = blk * 64 + q + h;
+            const double x = f < total ? F[(f % n) * r + f / n] / safe : 0.0;
+            int best = 0;
+            double bd = fabs(x - NF4_CB[0]);
+            for (int t = 1; t < 16; t++) {
+                const double d = fabs(x - NF4_CB[t]);
+                if (d < bd) { bd = d; best = t; }
+            }
+            code[h] = (uint8_t)best;
+        }
+        out[blk * 32 + q / 2] = (uint8_t)(code[0] | (code[1] << 4));
+    }
+}
+
+__global__ void dequant_kernel(const void* __restrict__ data, const double* __restrict__ scales,
+                               int64_t n, int r, int mode, double* __restrict__ dq)
+{
+    const int64_t total = n * r;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double v;
+        if (mode == RFXC_Q_I8) {
+            v = (double)reinterpret_cast<const int8_t*>(data)[e] * scales[e % r];
+        } else if (mode == RFXC_Q_F32) {
+            v = (double)reinterpret_cast<const float*>(data)[e];
+        } else if (mode == RFXC_Q_F16) {
+            v = (double)__half2float(reinterpret_cast<const __half*>(data)[e]);
+        } else {
+            const int64_t i = e / r, c = e % r;
+            const int64_t f = c * n + i;
+            const uint8_t byte = reinterpret_cast<const uint8_t*>(data)[f >> 1];
+            const int code = (f & 1) ? (byte >> 4) : (byte & 0x0F);
+            v = NF4_CB[code] * scales[f / 64];
+        }
+        dq[e] = v;
+    }
+}
+
+// pmax: block q < nparts -> max of diag over its rows; last block -> the
+// 1024 sampled pairs (Pcg32(seed, SEQ_PMAX), i == j skipped, no redraw).
+__global__ void __launch_bounds__(256)
+pmax_kernel(const double* __restrict__ dq, int64_t n, int r, int64_t rows_per_part, int nparts,
+            uint64_t s0, uint64_t s1, double* __restrict__ parts)
+{
+    __shared__ double red[32];
+    __shared__ int pairs[2048];
+    double m = -INFINITY;
+    if ((int)blockIdx.x < nparts) {
+        const int64_t r0 = blockIdx.x * rows_per_part, r1 = min(n, r0 + rows_per_part);
+        for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+            double s = 0.0;
+            for (int c = 0; c < r; c++) s += dq[i * r + c] * dq[i * r + c];
+            m = fmax(m, s);
+        }
+    } else {
+        if (threadIdx.x == 0) {
+            uint64_t s[2] = {s0, s1};
+            for (int t = 0; t < 1024; t++) {
+                pairs[2 * t] = (int)rfx_pcg32_bounded(s, (uint32_t)n);
+                pairs[2 * t + 1] = (int)rfx_pcg32_bounded(s, (uint32_t)n);
+            }
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < 1024; t += blockDim.x) {
+            const int64_t i = pairs[2 * t], j = pairs[2 * t + 1];
+            if (i == j) continue;
+            double s = 0.0;
+            for (int c = 0; c < r; c++) s += dq[i * r + c] * dq[j * r + c];
+            m = fmax(m, s);
+        }
+    }
+    m = block_max(m, red);
+    if (threadIdx.x == 0) parts[blockIdx.x] = m;
+}
+
+__global__ void max_final_kernel(const double* __restrict__ parts, int np, double* out)
+{
+    if (threadIdx.x != 0) return;
+    double m = parts[0];
+    for (int q = 1; q < np; q++) m = fmax(m, parts[q]);
+    *out = m;
+}
+
+}  // namespace rfxc
+
+using namespace rfxc;
+
+extern "C" int rfxc_factor_quantize(const double* d_Q, int64_t n, int32_t k, const double* d_Wr,
+                                    int32_t r, int32_t mode, double* d_factor,
+                                    double* d_colmax_parts, double* d_scales, void* d_data,
+                                    void* stream)
+{
+    if (n < 1 || k < 1 || r < 1 || r > 256) return fail(RFXC_EDATA, "factor_quantize: bad shape");
+    cudaStream_t st = as_stream(stream);
+    const int parts = gram_parts(n);
+    const int64_t rpp = ceil_div(n, parts);
+    const int threads = 256;
+    const size_t smem = ((size_t)k * r + threads) * 8;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    factor_kernel<<<parts, threads, smem, st>>>(d_Q, n, k, d_Wr, r, rpp, d_factor, d_colmax_parts);
+    int rc = check_launch("factor");
+    if (rc) return rc;
+    const int64_t total = n * r;
+    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 16);
+    switch (mode) {
+    case RFXC_Q_I8:
+        colmax_final_kernel<<<(unsigned)ceil_div(r, 128), 128, 0, st>>>(d_colmax_parts, parts, r,
+                                                                        d_scales);
+        quant_i8_kernel<<<grid, 256, 0, st>>>(d_factor, total, r, d_scales,
+                                              reinterpret_cast<int8_t*>(d_data));
+        break;
+    case RFXC_Q_F32:
+    case RFXC_Q_F16:
+        quant_cast_kernel<<<grid, 256, 0, st>>>(d_factor, total, mode, d_data);
+        break;
+    case RFXC_Q_NF4: {
+        const int64_t nb = ceil_div(total, 64);
+        quant_nf4_kernel<<<(unsigned)ceil_div(nb, 128), 128, 0, st>>>(
+            d_factor, n, r, nb, d_scales, reinterpret_cast<uint8_t*>(d_data));
+        break;
+    }
+    default:
+        return fail(RFXC_EDATA, "factor_quantize: unknown mode %d", mode);
+    }
+    return check_launch("quantize");
+}
+
+extern "C" int rfxc_dequantize(const void* d_data, const double* d_scales, int64_t n, int32_t r,
+                               int32_t mode, double* d_dq, void* stream)
+{
+    if (n < 1 || r < 1 || mode < 0 || mode > RFXC_Q_NF4) return fail(RFXC_EDATA, "dequantize");
+    const int grid = (int)std::min<int64_t>(ceil_div(n * r, 256), (int64_t)sm_count() * 16);
+    dequant_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_data, d_scales, n, r, mode, d_dq);
+    return check_launch("dequantize");
+}
+
+extern "C" int rfxc_pmax(const double* d_dq, int64_t n, int32_t r, int64_t seed, double* d_parts,
+                         double* d_out, void* stream)
+{
+    if (n < 1 || r < 1) return fail(RFXC_EDATA, "pmax: bad shape");
+    if (n > UINT32_MAX) return fail(RFXC_EDATA, "pmax: n exceeds uint32");
+    cudaStream_t st = as_stream(stream);
+    const int parts = gram_parts(n);
+    const int64_t rpp = ceil_div(n, parts);
+    uint64_t s[2];
+    rfx_pcg32_make(seed, RFX_SEQ_PMAX, s);
+    pmax_kernel<<<parts + 1, 256, 0, st>>>(d_dq, n, r, rpp, parts, s[0], s[1], d_parts);
+    int rc = check_launch("pmax");
+    if (rc) return rc;
+    max_final_kernel<<<1, 32, 0, st>>>(d_parts, parts + 1, d_out);
+    return check_launch("pmax_final");
+}

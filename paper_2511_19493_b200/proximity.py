@@ -1,0 +1,647 @@
+"""Proximity backends — drop-in for the reference's proximity.py hot path.
+
+Same function names, signatures, defaults, dataclasses and error behaviour as
+``rfx.proximity`` (proximity.py:68-420); the bodies call the sm_100a kernels
+of librfxc.so through the C ABI (include/rfxc.h).  There is no CPU fallback:
+without a CUDA device or the built library every call raises RfxError.
+
+Results stay on the device between calls (``LeafMembership`` keeps its codes
+and leaf buckets in HBM; ``FullTriangle.packed`` / ``LeafMembership.codes``
+are copied to the host only when read), so
+``lowrank_proximity(leaf_membership(forest, ds), ...)`` never round-trips the
+(n, B) codes through the host.
+
+Tree sharding (multi-GPU): ``leaf_membership(..., trees=(lo, hi))``
+builds a shard; ``lowrank_proximity`` on a shard all-reduces the (n, k)
+sketch partials with torch.distributed (NCCL) — the only collective.
+"""
+
+from __future__ import annotations
+
+import logging
+from collections.abc import Mapping
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .device import DeviceForest, DeviceMembership, DeviceValues, traverse
+from .errors import BudgetError, DataError, RfxError
+from .quantize import (BYTES_PER_ELEMENT, MODES, QuantFactor, dequantize,
+                       device_dequantize, factor_quantize, to_host)
+
+logger = logging.getLogger(__name__)
+
+ZERO_TIER = 1e-6          # proximity.py:39
+DEFAULT_TAU = 1e-4        # proximity.py:43
+DEFAULT_BUDGET = 32 * 2**30
+DEFAULT_RETENTION = 0.8
+_OVERSAMPLE = 8           # proximity.py:51
+_POWER_ITERS = 2          # proximity.py:52
+SEQ_FACTOR, SEQ_PMAX = 3, 4
+
+
+def _packed_len(n: int) -> int:
+    return n * (n - 1) // 2
+
+
+def _row_start(n: int, i: int) -> int:
+    """Packed index of (i, i+1); _row_start(n, n) == n(n-1)/2."""
+    return i * (2 * n - i - 1) // 2
+
+
+def packed_index(n: int, i, j):
+    """Index of (i, j), i < j, in the row-major packed upper triangle."""
+    return i * (2 * n - i - 1) // 2 + (j - i - 1)
+
+
+def _check_pair(n, i, j):
+    i, j = int(i), int(j)
+    if not (0 <= i < n and 0 <= j < n):
+        raise IndexError(f"pair ({i}, {j}) out of range for n={n}")
+    return (j, i) if i > j else (i, j)
+
+
+# ---------------------------------------------------------------- membership
+class LeafMembership:
+    """Terminal-leaf code of every sample in every tree (proximity.py:68-97).
+
+    Constructible from host arrays exactly like the reference dataclass;
+    when produced by ``leaf_membership`` the codes live on the GPU and
+    ``codes`` is materialised on first read."""
+
+    def __init__(self, codes=None, leaf_counts=None, *, _dev: DeviceMembership | None = None):
+        self._codes = None if codes is None else np.asarray(codes)
+        self.leaf_counts = np.asarray(leaf_counts, dtype=np.int32)
+        self._dev = _dev
+
+    @property
+    def codes(self) -> np.ndarray:
+        if self._codes is None:
+            d = self._dev
+            if d.is_shard:
+                raise RfxError("codes of a tree shard: gather with "
+                               "distributed.gather_codes(membership)")
+            self._codes = d.codes_nb.cpu().numpy()
+        return self._codes
+
+    @codes.setter
+    def codes(self, value):
+        self._codes = np.asarray(value)
+        self._dev = None
+
+    @property
+    def n(self) -> int:
+        return self._dev.n if self._dev is not None else self._codes.shape[0]
+
+    @property
+    def tree_count(self) -> int:
+        return self._dev.B if self._dev is not None else self._codes.shape[1]
+
+    @property
+    def total_leaves(self) -> int:
+        return int(self.leaf_counts.sum())
+
+    @property
+    def tree_range(self):
+        d = self._dev
+        return (0, self.tree_count) if d is None else (d.tree_lo, d.tree_hi)
+
+    def device(self) -> DeviceMembership:
+        if self._dev is None:
+            self._dev = DeviceMembership.from_host(self._codes, self.leaf_counts)
+        return self._dev
+
+    def onehot(self):
+        """Host CSR one-hot (proximity.py:88-97) for API parity; the device
+        path never builds it."""
+        import scipy.sparse as sp
+        codes = self.codes
+        n, B = codes.shape
+        off = np.zeros(B + 1, dtype=np.int64)
+        off[1:] = np.cumsum(self.leaf_counts)
+        cols = (codes.astype(np.int64) + off[:B][None, :]).reshape(-1)
+        rows = np.repeat(np.arange(n, dtype=np.int64), B)
+        return sp.csr_matrix((np.full(n * B, 1.0 / np.sqrt(B)), (rows, cols)),
+                             shape=(n, int(off[B])))
+
+    def __repr__(self):
+        return f"LeafMembership(n={self.n}, tree_count={self.tree_count})"
+
+
+def leaf_membership(forest, dataset, trees: tuple | None = None) -> LeafMembership:
+    """Classify every sample down every tree on the GPU (proximity.py:100-116).
+
+    ``trees=(lo, hi)`` restricts the work to a tree shard (multi-GPU)."""
+    if forest.n != dataset.n or forest.p != dataset.p:
+        raise DataError("forest and dataset shapes disagree")
+    B = forest.ntree
+    lo, hi = (0, B) if trees is None else (int(trees[0]), int(trees[1]))
+    if not 0 <= lo < hi <= B:
+        raise DataError(f"tree range {trees} outside [0, {B})")
+    dforest = DeviceForest(forest, lo, hi)
+    dvals = DeviceValues(dataset.values)
+    nb, tm, _ = traverse(dforest, dvals)
+    dev = DeviceMembership(nb, tm, dforest.leaf_counts, lo, hi, B)
+    if lo == 0 and hi == B:
+        lc = dforest.leaf_counts
+    else:
+        lc = np.array([int((np.asarray(t.status) == 1).sum()) for t in forest.trees],
+                      dtype=np.int32)
+    return LeafMembership(leaf_counts=lc, _dev=dev)
+
+
+# ------------------------------------------------------------- full triangle
+@dataclass
+class FullTriangle:
+    """Exact proximities, packed upper triangle, implicit unit diagonal
+    (proximity.py:123-146)."""
+
+    n: int
+    tree_count: int
+    packed: np.ndarray
+
+    def entry(self, i: int, j: int) -> float:
+        i, j = _check_pair(self.n, i, j)
+        if i == j:
+            return 1.0
+        return float(self.packed[packed_index(self.n, i, j)])
+
+    def to_dense(self) -> np.ndarray:
+        dense = np.empty((self.n, self.n), dtype=np.float64)
+        iu = np.triu_indices(self.n, k=1)
+        dense[iu] = self.packed
+        dense.T[iu] = self.packed
+        np.fill_diagonal(dense, 1.0)
+        return dense
+
+    def nbytes(self) -> int:
+        return self.packed.nbytes
+
+
+def _device_budget(nbytes: int, what: str, n: int, B: int):
+    import torch
+    free, _total = torch.cuda.mem_get_info()
+    if nbytes > free:
+        raise BudgetError(f"{what} for n={n} needs {nbytes} bytes of device memory, "
+                          f"{free} free; shard rows across GPUs or use the lowrank backend",
+                          memory_plan(n, tree_count=B))
+
+
+def pair_counts_device(membership: LeafMembership, layout: int, row_lo: int = 0,
+                       row_hi: int | None = None):
+    """K3 on the device: returns the output tensor for rows [row_lo, row_hi)."""
+    import torch
+    d = membership.device()
+    if d.is_shard:
+        raise DataError("pair counts need every tree's codes (row-shard instead)")
+    n, B = d.n, d.B
+    row_hi = n if row_hi is None else row_hi
+    if layout == _lib.BLOCK_I32:
+        numel, dt = (row_hi - row_lo) * n, torch.int32
+    else:
+        numel = _row_start(n, row_hi) - _row_start(n, row_lo)
+        dt = torch.float64 if layout == _lib.UPPER_F64 else torch.int32
+    _device_budget(numel * (8 if dt == torch.float64 else 4), "pair counts", n, B)
+    out = torch.empty(max(numel, 1), dtype=dt, device=d.codes_nb.device)
+    if n >= 2 and row_hi > row_lo:
+        _lib.call("rfxc_pair_counts", _lib.ptr(d.codes_nb), n, B, row_lo, row_hi, layout,
+                  _lib.ptr(out), _lib.stream_handle())
+    return out[:numel]
+
+
+def full_proximity(membership: LeafMembership,
+                   budget_bytes: int | None = DEFAULT_BUDGET) -> FullTriangle:
+    """p(i, j) = (1/B) #{trees with node_b(i) = node_b(j)}, exact
+    (proximity.py:188-201); the count/B division runs in the kernel
+    epilogue as an IEEE f64 division."""
+    n = membership.n
+    est = 8 * _packed_len(n)
+    if budget_bytes is not None and est > budget_bytes:
+        raise BudgetError(
+            f"full proximity for n={n} needs {est} bytes (packed), over the "
+            f"{budget_bytes}-byte budget; consider the triblock or lowrank backend",
+            memory_plan(n, tree_count=membership.tree_count))
+    if n < 2:
+        return FullTriangle(n=n, tree_count=membership.tree_count,
+                            packed=np.empty(0, dtype=np.float64))
+    out = pair_counts_device(membership, _lib.UPPER_F64)
+    return FullTriangle(n=n, tree_count=membership.tree_count, packed=out.cpu().numpy())
+
+
+# ------------------------------------------------------------------ TriBlock
+class PairMap(Mapping):
+    """Read-only (i, j) -> value map over (i, j)-sorted arrays: the TriBlock
+    dense tier without a Python dict insert per pair (proximity.py:315-316).
+    Supports everything the reference does with the dict (get, [], len,
+    iteration, items, values, keys)."""
+
+    def __init__(self, n: int, i: np.ndarray, j: np.ndarray, v: np.ndarray):
+        self.n = n
+        self.i = np.asarray(i, dtype=np.int32)
+        self.j = np.asarray(j, dtype=np.int32)
+        self.v = np.asarray(v, dtype=np.float64)
+        self._key = self.i.astype(np.int64) * n + self.j
+
+    def _find(self, key):
+        try:
+            a, b = int(key[0]), int(key[1])
+        except (TypeError, ValueError, IndexError):
+            return -1
+        k = a * self.n + b
+        pos = int(np.searchsorted(self._key, k))
+        return pos if pos < len(self._key) and self._key[pos] == k else -1
+
+    def __getitem__(self, key):
+        pos = self._find(key)
+        if pos < 0:
+            raise KeyError(key)
+        return float(self.v[pos])
+
+    def __contains__(self, key):
+        return self._find(key) >= 0
+
+    def __len__(self):
+        return len(self._key)
+
+    def __iter__(self):
+        return zip(self.i.tolist(), self.j.tolist())
+
+    def items(self):
+        return zip(zip(self.i.tolist(), self.j.tolist()), self.v.tolist())
+
+    def values(self):
+        return self.v.tolist()
+
+
+@dataclass
+class TriBlock:
+    """Value-tiered proximity storage (proximity.py:208-272)."""
+
+    n: int
+    tree_count: int
+    tau: float
+    dense: Mapping
+    sparse_i: np.ndarray
+    sparse_j: np.ndarray
+    sparse_v: np.ndarray
+    _sparse_key: np.ndarray = field(default=None, repr=False)
+
+    def __post_init__(self):
+        if self._sparse_key is None:
+            self._sparse_key = self.sparse_i.astype(np.int64) * self.n + self.sparse_j
+
+    def entry(self, i: int, j: int) -> float:
+        i, j = _check_pair(self.n, i, j)
+        if i == j:
+            return 1.0
+        v = self.dense.get((i, j))
+        if v is not None:
+            return float(v)
+        key = i * self.n + j
+        pos = np.searchsorted(self._sparse_key, key)
+        if pos < len(self._sparse_key) and self._sparse_key[pos] == key:
+            return float(self.sparse_v[pos])
+        return 0.0
+
+    @property
+    def dense_count(self) -> int:
+        return len(self.dense)
+
+    @property
+    def sparse_count(self) -> int:
+        return len(self.sparse_v)
+
+    @property
+    def stored_pairs(self) -> int:
+        return self.dense_count + self.sparse_count
+
+    def compression_ratio(self) -> float:
+        return _packed_len(self.n) / max(self.stored_pairs, 1)
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros((self.n, self.n), dtype=np.float64)
+        if isinstance(self.dense, PairMap):
+            di, dj, dv = self.dense.i, self.dense.j, self.dense.v
+        else:
+            keys = list(self.dense)
+            di = np.array([k[0] for k in keys], dtype=np.int64)
+            dj = np.array([k[1] for k in keys], dtype=np.int64)
+            dv = np.array([self.dense[k] for k in keys], dtype=np.float64)
+        out[di, dj] = dv
+        out[dj, di] = dv
+        out[self.sparse_i, self.sparse_j] = self.sparse_v
+        out[self.sparse_j, self.sparse_i] = self.sparse_v
+        np.fill_diagonal(out, 1.0)
+        return out
+
+    def nbytes(self) -> int:
+        return self.dense_count * 16 + self.sparse_count * 16
+
+
+def _scan(x):
+    import torch
+    out = torch.empty_like(x)
+    tot = torch.empty(1, dtype=torch.int64, device=x.device)
+    _lib.call("rfxc_exclusive_scan_i64", _lib.ptr(x), x.numel(), _lib.ptr(out), _lib.ptr(tot),
+              _lib.stream_handle())
+    return out, tot
+
+
+def triblock_proximity(membership: LeafMembership, tau: float = DEFAULT_TAU,
+                       budget_bytes: int | None = DEFAULT_BUDGET) -> TriBlock:
+    """Same values as full_proximity routed into tiers (proximity.py:275-327):
+    int32 count tiles on the device, then a count / scan / emit compaction
+    that writes both tiers already sorted by (i, j)."""
+    import torch
+    if not (ZERO_TIER < tau < 1.0):
+        raise DataError(f"tau must lie in ({ZERO_TIER}, 1), got {tau}")
+    n, B = membership.n, membership.tree_count
+    est = int(8 * n * n * 0.5 * DEFAULT_RETENTION)
+    if budget_bytes is not None and est > budget_bytes:
+        raise BudgetError(
+            f"triblock proximity for n={n} estimates {est} bytes, over the "
+            f"{budget_bytes}-byte budget; consider the lowrank backend",
+            memory_plan(n, tree_count=B))
+    empty_i = np.empty(0, dtype=np.int32)
+    if n < 2:
+        return TriBlock(n, B, tau, PairMap(n, empty_i, empty_i, np.empty(0)), empty_i,
+                        empty_i, np.empty(0))
+    d = membership.device()
+    dev = d.codes_nb.device
+    # row blocks bounded to ~1 G int32 counters each
+    hot, cold = [], []
+    lo = 0
+    while lo < n - 1:
+        a, b = lo + 1, n  # largest hi with at most 2^30 counters (at least one row)
+        while a < b:
+            mid = (a + b + 1) // 2
+            if _row_start(n, mid) - _row_start(n, lo) <= (1 << 30):
+                a = mid
+            else:
+                b = mid - 1
+        hi = a
+        counts = pair_counts_device(membership, _lib.UPPER_I32, lo, hi)
+        rows = hi - lo
+        rc = torch.empty(2 * rows, dtype=torch.int64, device=dev)
+        _lib.call("rfxc_triblock_count", _lib.ptr(counts), n, B, lo, hi, float(tau), _lib.ptr(rc),
+                  _lib.stream_handle())
+        oh, th = _scan(rc[:rows])
+        oc, tc = _scan(rc[rows:])
+        nh, nc = int(th.item()), int(tc.item())
+        offs = torch.cat([oh, oc])
+        hi_i = torch.empty(max(nh, 1), dtype=torch.int32, device=dev)
+        hi_j = torch.empty(max(nh, 1), dtype=torch.int32, device=dev)
+        hi_v = torch.empty(max(nh, 1), dtype=torch.float64, device=dev)
+        co_i = torch.empty(max(nc, 1), dtype=torch.int32, device=dev)
+        co_j = torch.empty(max(nc, 1), dtype=torch.int32, device=dev)
+        co_v = torch.empty(max(nc, 1), dtype=torch.float64, device=dev)
+        _lib.call("rfxc_triblock_emit", _lib.ptr(counts), n, B, lo, hi, float(tau),
+                  _lib.ptr(offs), _lib.ptr(hi_i), _lib.ptr(hi_j), _lib.ptr(hi_v),
+                  _lib.ptr(co_i), _lib.ptr(co_j), _lib.ptr(co_v), _lib.stream_handle())
+        hot.append((hi_i[:nh].cpu().numpy(), hi_j[:nh].cpu().numpy(), hi_v[:nh].cpu().numpy()))
+        cold.append((co_i[:nc].cpu().numpy(), co_j[:nc].cpu().numpy(), co_v[:nc].cpu().numpy()))
+        del counts
+        lo = hi
+    cat = lambda parts, q: np.concatenate([p[q] for p in parts])
+    dense = PairMap(n, cat(hot, 0), cat(hot, 1), cat(hot, 2))
+    return TriBlock(n=n, tree_count=B, tau=tau, dense=dense, sparse_i=cat(cold, 0),
+                    sparse_j=cat(cold, 1), sparse_v=cat(cold, 2))
+
+
+# ------------------------------------------------------------------ low rank
+@dataclass
+class LowRankQuantized:
+    """Symmetric factorisation P ~ Q Q^T with Q quantised (proximity.py:334-364).
+    ``_dq_dev`` keeps the dequantised factor on the GPU for mds_lowrank."""
+
+    n: int
+    rank: int
+    mode: str
+    factor: QuantFactor
+    pmax: float
+    tree_count: int
+    rank_degraded: bool = False
+    _dq: np.ndarray = field(default=None, repr=False)
+    _dq_dev: object = field(default=None, repr=False)
+
+    def dequantized(self) -> np.ndarray:
+        if self._dq is None:
+            self._dq = self.factor.dequantize()
+        return self._dq
+
+    def dequantized_device(self):
+        """(n, r) f64 dequantised factor on the GPU."""
+        import torch
+        if self._dq_dev is None:
+            dev = _lib.require_cuda()
+            data = torch.from_numpy(np.ascontiguousarray(self.factor.data)).to(dev)
+            sc = None if self.factor.scales is None else torch.from_numpy(
+                np.ascontiguousarray(self.factor.scales)).to(dev)
+            n, r = self.n, int(np.prod(self.factor.shape)) // max(self.n, 1)
+            self._dq_dev = device_dequantize(data, sc, n, r, self.mode)
+        return self._dq_dev
+
+    def entry(self, i: int, j: int) -> float:
+        i, j = _check_pair(self.n, i, j)
+        if i == j:
+            return 1.0
+        Q = self.dequantized()
+        return float(np.clip(Q[i] @ Q[j], 0.0, 1.0))
+
+    def nbytes(self) -> int:
+        return self.factor.payload_nbytes()
+
+
+class _Sketch:
+    """P X for the (local trees of the) membership: leaf sums + gather, and
+    the all-reduce of the partials when the membership is a tree shard."""
+
+    def __init__(self, d: DeviceMembership, k: int, group=None):
+        import torch
+        self.d = d
+        self.k = k
+        self.ld = (k + 3) // 4 * 4
+        self.perm, self.seg = d.buckets()
+        dev = d.codes_nb.device
+        self.S = torch.empty((max(d.total_leaves, 1), self.ld), dtype=torch.float32, device=dev)
+        self.group = group
+
+    def apply(self, X32, kk: int, reduce: bool = True):
+        """P X as (n, kk) f64; X32 is the (n, ld) f32 copy of X (zero beyond kk)."""
+        import torch
+        d = self.d
+        Y = torch.empty((d.n, kk), dtype=torch.float64, device=X32.device)
+        _lib.call("rfxc_leaf_sums", _lib.ptr(self.perm), _lib.ptr(self.seg), 0, d.total_leaves,
+                  _lib.ptr(X32), kk, self.ld, _lib.ptr(self.S), _lib.stream_handle())
+        _lib.call("rfxc_leaf_gather", _lib.ptr(d.codes_nb), d.n, d.Bl, _lib.ptr(d.leaf_base),
+                  _lib.ptr(self.S), kk, self.ld, 1.0 / d.B, 0, _lib.ptr(Y),
+                  _lib.stream_handle())
+        if d.is_shard and reduce:
+            import torch.distributed as dist
+            dist.all_reduce(Y, op=dist.ReduceOp.SUM, group=self.group)
+        return Y
+
+
+def _gram(A, Bm):
+    import torch
+    n, ka = A.shape
+    kb = Bm.shape[1]
+    parts = torch.empty(_lib.load().rfxc_gram_parts(n) * ka * kb, dtype=torch.float64,
+                        device=A.device)
+    C = torch.empty((ka, kb), dtype=torch.float64, device=A.device)
+    _lib.call("rfxc_gram", _lib.ptr(A), _lib.ptr(Bm), n, ka, kb, _lib.ptr(parts), _lib.ptr(C),
+              _lib.stream_handle())
+    return C.cpu().numpy()
+
+
+def _times(Y, M, ld32):
+    """(Y @ M) on the device, f64 plus the padded f32 sketch operand."""
+    import torch
+    n, ka = Y.shape
+    kb = M.shape[1]
+    m = torch.from_numpy(np.ascontiguousarray(M, dtype=np.float64)).to(Y.device)
+    Z = torch.empty((n, kb), dtype=torch.float64, device=Y.device)
+    Z32 = torch.empty((n, max(ld32, 4)), dtype=torch.float32, device=Y.device)
+    _lib.call("rfxc_matmul_small", _lib.ptr(Y), n, ka, _lib.ptr(m), kb, _lib.ptr(Z),
+              _lib.ptr(Z32), Z32.shape[1], _lib.stream_handle())
+    return Z, Z32
+
+
+def orthonormalize(Y, ld: int):
+    """Orthonormal basis of range(Y) (the np.linalg.qr of proximity.py:395,
+    :397) as Gram-eigen + Cholesky QR on the device: G = Y^T Y (device
+    skinny reduction), host k x k eigh / Cholesky, Q = Y M (device).
+    Directions below the f64 noise floor of G are dropped (k' <= k).
+    Returns (Q f64 (n, k'), Q32 f32 (n, ld'))."""
+    G = _gram(Y, Y)
+    lam, V = np.linalg.eigh(0.5 * (G + G.T))
+    top = lam.max() if lam.size else 0.0
+    keep = lam > max(top, 0.0) * 1e-13
+    if not keep.any():
+        keep = np.zeros_like(keep)
+        keep[-1] = True
+        lam = np.maximum(lam, 1e-300)
+    M1 = V[:, keep] / np.sqrt(lam[keep])[None, :]
+    M1 = M1[:, ::-1].copy()  # strongest direction first
+    kk = M1.shape[1]
+    Q1, _ = _times(Y, M1, ld)
+    G2 = _gram(Q1, Q1)
+    R = np.linalg.cholesky(0.5 * (G2 + G2.T)).T  # G2 = R^T R
+    Rinv = np.linalg.solve(R, np.eye(kk))
+    return _times(Q1, Rinv, ld)
+
+
+def lowrank_proximity(membership: LeafMembership, rank: int, mode: str = "i8",
+                      seed: int = 0, group=None) -> LowRankQuantized:
+    """Randomised symmetric rank-r factorisation of P = M M^T followed by
+    quantisation (proximity.py:367-420), with P applied implicitly on the
+    GPU (K4) and never materialised."""
+    import torch
+    if mode not in MODES:
+        raise DataError(f"unknown quantization mode {mode!r}")
+    n = membership.n
+    if rank < 1:
+        raise DataError(f"rank must be >= 1, got {rank}")
+    bound = min(n, membership.total_leaves)
+    degraded = rank > bound
+    if degraded:
+        logger.warning("requested rank %d exceeds membership rank bound %d; "
+                       "degrading to the exact bound", rank, bound)
+    r = min(rank, bound)
+    d = membership.device()
+    dev = d.codes_nb.device
+    k = min(n, r + _OVERSAMPLE)
+    sk = _Sketch(d, k, group)
+    ld = sk.ld
+    omega = torch.empty((n, k), dtype=torch.float64, device=dev)
+    _lib.call("rfxc_normals", seed, SEQ_FACTOR, n * k, _lib.ptr(omega), _lib.stream_handle())
+    X32 = torch.empty((n, ld), dtype=torch.float32, device=dev)
+    _lib.call("rfxc_pack_f32", _lib.ptr(omega), n, k, ld, _lib.ptr(X32), _lib.stream_handle())
+    # k' <= k columns survive a numerically rank-deficient basis; the f32
+    # operand keeps the padded stride ld either way
+    Q, Q32 = orthonormalize(sk.apply(X32, k), ld)
+    for _ in range(_POWER_ITERS):
+        Q, Q32 = orthonormalize(sk.apply(Q32, Q.shape[1]), ld)
+    Z = sk.apply(Q32, Q.shape[1])
+    T = _gram(Q, Z)
+    T = 0.5 * (T + T.T)
+    lam, W = np.linalg.eigh(T)
+    order = np.argsort(lam)[::-1][:r]
+    lam = np.clip(lam[order], 0.0, None)
+    Wr = W[:, order] * np.sqrt(lam)[None, :]
+    if Wr.shape[1] < r:  # numerically rank-deficient: zero factor columns
+        Wr = np.pad(Wr, ((0, 0), (0, r - Wr.shape[1])))
+    data, scales = factor_quantize(Q, Wr, mode)
+    dq = device_dequantize(data, scales, n, r, mode)
+    parts = torch.empty(_lib.load().rfxc_gram_parts(n) + 1, dtype=torch.float64, device=dev)
+    pm = torch.empty(1, dtype=torch.float64, device=dev)
+    _lib.call("rfxc_pmax", _lib.ptr(dq), n, r, seed, _lib.ptr(parts), _lib.ptr(pm),
+              _lib.stream_handle())
+    qf = to_host(mode, (n, r), data, scales)
+    return LowRankQuantized(n=n, rank=r, mode=mode, factor=qf, pmax=float(pm.item()),
+                            tree_count=membership.tree_count, rank_degraded=degraded,
+                            _dq_dev=dq)
+
+
+# ------------------------------------------------------------------ accessors
+def entry(repr_, i: int, j: int) -> float:
+    return repr_.entry(i, j)
+
+
+# ------------------------------------------------------------------- planner
+PLAN_MAXNODE, PLAN_FEATURES, PLAN_CLASSES = 1000, 50, 3
+GiB = 2**30
+
+
+def memory_plan(n: int, tree_count: int | None = None, rank: int | None = None,
+                mode: str | None = None, backend: str | None = None,
+                retention: float = DEFAULT_RETENTION, n_features: int = PLAN_FEATURES,
+                maxnode: int = PLAN_MAXNODE, n_classes: int = PLAN_CLASSES) -> dict:
+    """Closed-form byte counts and feasibility verdicts, same keys and
+    arithmetic as the reference planner (proximity.py:500-595); carried by
+    BudgetError."""
+    if n < 1:
+        raise DataError("memory_plan needs n >= 1")
+    square = 8 * n * n
+    tri = int(square * 0.5 * retention)
+
+    def lr(rk, m):
+        return {"two_factor": int(2 * n * rk * BYTES_PER_ELEMENT[m]),
+                "single_factor": int(n * rk * BYTES_PER_ELEMENT[m])}
+
+    table = {m: lr(32, m) for m in MODES}
+    B = tree_count if tree_count is not None else 10_000
+    model = {"training_data": n * n_features * 4, "tree_structures": 2 * maxnode * B * 4,
+             "node_status": maxnode * B * 4, "split_values": maxnode * B * 4,
+             "split_variables": maxnode * B * 4, "node_classes": maxnode * B * 4,
+             "class_populations": n_classes * maxnode * B * 4,
+             "oob_tracking": n * n_classes * 4}
+    model["subtotal"] = sum(model.values())
+    imp = {"overall": n_features * 4, "local_per_sample": n * 4,
+           "local_matrix": n * n_features * 4, "importance_sd": n_features * 4}
+    imp["subtotal"] = sum(imp.values())
+    cand = {"full": square, "triblock": tri, "lowrank_i8_r32": table["i8"]["two_factor"],
+            "lowrank_nf4_r32": table["nf4"]["two_factor"]}
+    f32g = {k_: v <= 0.8 * 32 * GiB for k_, v in cand.items()}
+    f12g = {k_: v <= 0.8 * 12 * GiB for k_, v in cand.items()}
+    if n <= 5000:
+        rec = "full or triblock"
+    elif f32g["triblock"]:
+        rec = "triblock"
+    else:
+        rec = "lowrank (i8 for speed, nf4 for minimum memory)"
+    plan = {"samples": n, "trees": B, "full_headline_bytes": square,
+            "full_packed_bytes": 8 * _packed_len(n), "triblock_bytes": tri,
+            "triblock_retention": retention, "lowrank_r32_bytes": table, "model": model,
+            "importance": imp, "feasible_32gb": f32g, "feasible_12gb": f12g,
+            "recommended": rec}
+    if rank is not None and mode is not None:
+        req = lr(rank, mode)
+        plan["requested"] = {"backend": backend or "lowrank", "rank": rank, "mode": mode,
+                             "bytes": req, "compression_vs_full": square / max(req["two_factor"], 1)}
+    elif backend in ("full", "triblock"):
+        chosen = {"full": 8 * _packed_len(n), "triblock": tri}[backend]
+        plan["requested"] = {"backend": backend, "bytes": {"stored": chosen},
+                             "compression_vs_full": square / max(chosen, 1)}
+    return plan

@@ -1,0 +1,124 @@
+"""K2/K3 parity: co-occurrence counts are bit-exact with the reference."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_2511_19493_b200 import _lib
+from paper_2511_19493_b200 import proximity as P
+
+pytestmark = pytest.mark.gpu
+
+
+def brute(codes):
+    n, B = codes.shape
+    M = np.zeros((n, n))
+    for b in range(B):
+        c = codes[:, b]
+        M += c[:, None] == c[None, :]
+    return M / B
+
+
+def test_random_fixtures_exact():
+    # tests/test_proximity.py:74-87 and acceptance A5
+    for seed in (0, 42):
+        rng = np.random.default_rng(seed)
+        for _ in range(20):
+            n = int(rng.integers(5, 51))
+            B = int(rng.integers(1, 21))
+            codes = np.zeros((n, B), np.int32)
+            lc = np.zeros(B, np.int32)
+            for b in range(B):
+                k = int(rng.integers(1, max(2, n // 2 + 1)))
+                codes[:, b] = rng.integers(0, k, size=n)
+                lc[b] = codes[:, b].max() + 1 + int(rng.integers(0, 2))  # may exceed max+1
+            full = P.full_proximity(P.LeafMembership(codes, lc))
+            assert np.array_equal(full.to_dense(), brute(codes))
+
+
+def test_simple_pair_values():
+    full = P.full_proximity(P.LeafMembership(np.array([[0], [0], [1]], np.int32),
+                                             np.array([2], np.int32)))
+    assert full.entry(0, 1) == 1.0 and full.entry(0, 2) == 0.0
+    full2 = P.full_proximity(P.LeafMembership(np.array([[0, 0], [0, 1]], np.int32),
+                                              np.array([2, 2], np.int32)))
+    assert full2.entry(0, 1) == 0.5
+
+
+def test_wine_counts_and_packed_bit_exact(wine50, wine_ds):
+    g = golden("wine50.npz")
+    mem = P.leaf_membership(wine50, wine_ds)
+    full = P.full_proximity(mem)
+    assert np.array_equal(full.packed, g["packed"])
+    counts = P.pair_counts_device(mem, _lib.UPPER_I32).cpu().numpy()
+    assert np.array_equal(counts.astype(np.int64), g["pair_counts"])
+
+
+def test_synth2k_counts_sha(synth2k, fixtures):
+    ds, forest = synth2k
+    mem = P.leaf_membership(forest, ds)
+    counts = P.pair_counts_device(mem, _lib.UPPER_I32).cpu().numpy()
+    assert hashlib.sha256(counts.tobytes()).hexdigest() == fixtures["synth2k"]["counts_i32_sha"]
+
+
+def test_row_block_layouts(orc):
+    g = golden("synth2k.npz")
+    codes, lc = g["codes"], g["leaf_counts"]
+    mem = P.LeafMembership(codes, lc)
+    n = codes.shape[0]
+    full = P.pair_counts_device(mem, _lib.UPPER_I32).cpu().numpy()
+    for lo, hi in [(0, 1), (5, 300), (1234, 1999), (1998, 2000), (700, 2000)]:
+        blk = P.pair_counts_device(mem, _lib.BLOCK_I32, lo, hi).cpu().numpy().reshape(hi - lo, n)
+        assert np.array_equal(blk, orc.block_counts(codes, lc, lo, hi))
+        up = P.pair_counts_device(mem, _lib.UPPER_I32, lo, hi).cpu().numpy()
+        s, e = P._row_start(n, lo), P._row_start(n, hi)
+        assert np.array_equal(up, full[s:e])
+
+
+def test_triblock_matches_reference(wine50, wine_ds):
+    g = golden("wine50.npz")
+    mem = P.leaf_membership(wine50, wine_ds)
+    tb = P.triblock_proximity(mem, tau=0.05)
+    assert np.array_equal(tb.dense.i, g["tb_dense_i"]) and np.array_equal(tb.dense.j, g["tb_dense_j"])
+    assert np.array_equal(tb.dense.v, g["tb_dense_v"])
+    assert np.array_equal(tb.sparse_i, g["tb_sparse_i"])
+    assert np.array_equal(tb.sparse_j, g["tb_sparse_j"])
+    assert np.array_equal(tb.sparse_v, g["tb_sparse_v"])
+    assert all(v >= 0.05 for v in tb.dense.values())
+    full = P.full_proximity(mem)
+    tb2 = P.triblock_proximity(mem)  # default tau: every non-zero is dense (B < 1e4)
+    assert tb2.sparse_count == 0
+    assert np.array_equal(tb2.to_dense(), full.to_dense())
+
+
+def test_triblock_all_one_leaf(wine_ds, built):
+    from paper_2511_19493_b200.forest import TrainConfig, train
+    f = train(wine_ds, TrainConfig(ntree=2, iseed=1, min_node_size=10**6))
+    tb = P.triblock_proximity(P.leaf_membership(f, wine_ds), tau=0.5)
+    n = wine_ds.n
+    assert tb.dense_count == n * (n - 1) // 2 and tb.sparse_count == 0
+
+
+def test_one_tree_row_sum_equals_leaf_size():
+    codes = np.random.default_rng(4).integers(0, 6, size=(40, 1)).astype(np.int32)
+    dense = P.full_proximity(P.LeafMembership(codes, np.array([6], np.int32))).to_dense()
+    for i in range(40):
+        assert dense[i].sum() == pytest.approx((codes[:, 0] == codes[i, 0]).sum())
+
+
+def test_bucket_is_stable_counting_sort(synth2k):
+    ds, forest = synth2k
+    mem = P.leaf_membership(forest, ds)
+    d = mem.device()
+    perm, seg = d.buckets()
+    perm, seg = perm.cpu().numpy(), seg.cpu().numpy()
+    codes = golden("synth2k.npz")["codes"]
+    n = codes.shape[0]
+    for b in (0, 7, 39):
+        want = np.argsort(codes[:, b], kind="stable")
+        assert np.array_equal(perm[b], want)
+        lo, hi = d.leaf_base_host[b], d.leaf_base_host[b + 1]
+        starts = seg[lo:hi + 1] - b * n
+        assert np.array_equal(np.diff(starts), np.bincount(codes[:, b], minlength=hi - lo))

@@ -1,0 +1,130 @@
+"""Host-side logic: planner, tier map, relayout, sharding, validation."""
+
+import numpy as np
+import pytest
+
+from paper_2511_19493_b200 import distributed as D
+from paper_2511_19493_b200 import proximity as P
+from paper_2511_19493_b200.device import relayout_siblings
+from paper_2511_19493_b200.errors import BudgetError, DataError
+
+
+def test_planner_golden_rows():
+    # tests/test_proximity.py:280-321 / test_acceptance A4 of the reference
+    plan = P.memory_plan(100_000, tree_count=10_000)
+    assert plan["full_headline_bytes"] == 80_000_000_000
+    assert plan["triblock_bytes"] / 2**30 == pytest.approx(29.8, rel=0.02)
+    assert plan["lowrank_r32_bytes"]["i8"]["two_factor"] == 6_400_000
+    assert plan["lowrank_r32_bytes"]["nf4"]["two_factor"] == 3_200_000
+    assert plan["model"]["subtotal"] / 1e6 == pytest.approx(381.2, abs=0.1)
+    assert P.memory_plan(1_000)["recommended"] == "full or triblock"
+    assert P.memory_plan(50_000)["recommended"] == "triblock"
+    assert P.memory_plan(100_000)["recommended"].startswith("lowrank")
+    assert P.memory_plan(100_000, rank=32, mode="i8")["requested"]["bytes"]["two_factor"] \
+        == 6_400_000
+
+
+def test_budget_refusals_before_device_work():
+    mem = P.LeafMembership(np.zeros((1000, 1), np.int32), np.array([1], np.int32))
+    with pytest.raises(BudgetError) as e:
+        P.full_proximity(mem, budget_bytes=1000)
+    assert e.value.plan["samples"] == 1000
+    with pytest.raises(DataError):
+        P.triblock_proximity(mem, tau=1e-7)
+    with pytest.raises(DataError):
+        P.triblock_proximity(mem, tau=1.0)
+    with pytest.raises(DataError):
+        P.lowrank_proximity(mem, rank=0)
+    with pytest.raises(DataError):
+        P.lowrank_proximity(mem, rank=3, mode="q3")
+
+
+def test_packed_index_is_triu_order():
+    for n in (2, 3, 7, 20):
+        e = 0
+        for i in range(n):
+            for j in range(i + 1, n):
+                assert P.packed_index(n, i, j) == e
+                e += 1
+
+
+def test_pair_map_behaves_like_the_reference_dict():
+    i = np.array([0, 0, 2], np.int32)
+    j = np.array([1, 3, 3], np.int32)
+    v = np.array([0.5, 0.25, 1.0])
+    m = P.PairMap(4, i, j, v)
+    assert len(m) == 3 and m[(0, 3)] == 0.25 and m.get((1, 2)) is None
+    assert (2, 3) in m and (3, 2) not in m
+    assert dict(m.items()) == {(0, 1): 0.5, (0, 3): 0.25, (2, 3): 1.0}
+    assert set(m) == {(0, 1), (0, 3), (2, 3)} and sorted(m.values()) == [0.25, 0.5, 1.0]
+    tb = P.TriBlock(4, 2, 0.3, m, np.array([1], np.int32), np.array([2], np.int32),
+                    np.array([0.1]))
+    assert tb.entry(3, 2) == 1.0 and tb.entry(1, 2) == 0.1 and tb.entry(1, 3) == 0.0
+    assert tb.entry(1, 1) == 1.0 and tb.stored_pairs == 4
+    dense = tb.to_dense()
+    assert dense[3, 0] == 0.25 and dense[2, 1] == 0.1
+
+
+def test_full_triangle_accessors():
+    ft = P.FullTriangle(n=3, tree_count=2, packed=np.array([0.5, 0.0, 1.0]))
+    assert ft.entry(2, 1) == 1.0 and ft.entry(0, 0) == 1.0
+    with pytest.raises(IndexError):
+        ft.entry(0, 3)
+    assert ft.to_dense()[1, 0] == 0.5
+
+
+def _descend(st, sv, th, lf, rt, x):
+    node = 0
+    while st[node] == 0:
+        node = lf[node] if x[sv[node]] <= th[node] else (rt[node] if rt is not None
+                                                           else lf[node] + 1)
+    return node
+
+
+def test_relayout_keeps_routing_and_codes():
+    from conftest import golden
+    h = golden("handbuilt.npz")
+    st, sv, th, cm, lf, order = relayout_siblings(h["status"], h["split_var"], h["threshold"],
+                                                  np.zeros(7, np.int64), h["left"], h["right"])
+    internal = st == 0
+    assert np.all(lf[internal] >= 1)
+    ref_code = np.cumsum(h["status"] == 1) - 1
+    for x, want in zip(h["points"], h["codes"]):
+        node = _descend(st, sv, th, lf, None, x)
+        assert ref_code[order[node]] == want
+
+
+def test_tree_and_row_shards_cover_exactly():
+    for B, w in [(500, 8), (7, 3), (1000, 4)]:
+        s = [D.tree_shard(B, r, w) for r in range(w)]
+        assert s[0][0] == 0 and s[-1][1] == B
+        assert all(a[1] == b[0] for a, b in zip(s, s[1:]))
+        assert max(h - l for l, h in s) - min(h - l for l, h in s) <= 1
+    for n, w in [(50_000, 8), (10, 3), (200_000, 2)]:
+        s = [D.row_shard(n, r, w) for r in range(w)]
+        assert s[0][0] == 0 and s[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(s, s[1:]))
+        area = [P._row_start(n, h) - P._row_start(n, l) for l, h in s]
+        if n > 1000:
+            assert max(area) / min(area) < 1.01
+
+
+def test_leafmembership_mirrors_reference_dataclass():
+    codes = np.array([[0, 1], [0, 0], [1, 1]], np.int32)
+    mem = P.LeafMembership(codes=codes, leaf_counts=np.array([2, 2], np.int32))
+    assert mem.n == 3 and mem.tree_count == 2 and mem.total_leaves == 4
+    M = mem.onehot()
+    brute = sum((codes[:, b][:, None] == codes[:, b][None, :]) for b in range(2)) / 2
+    assert np.allclose((M @ M.T).toarray(), brute, atol=1e-12)
+
+
+def test_product_path_has_no_cpu_fallback(monkeypatch):
+    """Without a CUDA device the product raises instead of computing on CPU."""
+    import torch
+    from paper_2511_19493_b200.errors import RfxError
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    mem = P.LeafMembership(np.zeros((10, 2), np.int32), np.array([1, 1], np.int32))
+    with pytest.raises(RfxError):
+        P.full_proximity(mem)
+    with pytest.raises(RfxError):
+        P.lowrank_proximity(mem, rank=2)
