@@ -94,8 +94,23 @@ def check(rc: int, what: str = "") -> None:
     raise RfxError(text)
 
 
+# kernels launched per successful call (host-side count for bench.py's
+# gpu_launches; rfxc_gram / rfxc_mds_power add their data-dependent extras)
+LAUNCHES = {"rfxc_values_to_f32": 1, "rfxc_forest_pack": 1, "rfxc_leaf_codes": 1,
+            "rfxc_transpose_i32": 1, "rfxc_bucket": 1, "rfxc_pair_counts": 1,
+            "rfxc_triblock_count": 1, "rfxc_triblock_emit": 1, "rfxc_exclusive_scan_i64": 1,
+            "rfxc_normals": 1, "rfxc_pack_f32": 1, "rfxc_leaf_sums": 1, "rfxc_leaf_gather": 1,
+            "rfxc_gram": 2, "rfxc_matmul_small": 1, "rfxc_factor_quantize": 3,
+            "rfxc_dequantize": 1, "rfxc_pmax": 2, "rfxc_mds_power": 1, "rfxc_gram_matvec": 1}
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
     check(getattr(load(), name)(*args), name)
+    launch_count += LAUNCHES.get(name, 0)
+    if name == "rfxc_mds_power":
+        launch_count += int(args[4])  # start-vector normals, one per component
 
 
 def ptr(t) -> ctypes.c_void_p:

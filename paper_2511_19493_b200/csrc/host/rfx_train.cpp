@@ -316,12 +316,15 @@ extern "C" {
 
 const char* rfxt_last_error(void) { return g_err.c_str(); }
 
-// Grow `ntree` trees (forest.py:262-302).  Returns an opaque handle or NULL
-// (rfxt_last_error() says why).  nthreads <= 0 uses every core.
+// Grow trees [first_tree, first_tree + ntree) of a forest (forest.py:262-302;
+// tree t uses streams seeded iseed + t, so any tree range of the forest can
+// be grown independently — each GPU rank grows only its shard).  Returns an
+// opaque handle or NULL (rfxt_last_error() says why).  nthreads <= 0 uses
+// every core.  OOB votes cover the grown trees only.
 void* rfxt_train(const double* values, int64_t n, int32_t p, const int32_t* labels,
                  int32_t n_classes, const uint8_t* col_cat, const int32_t* col_levels,
-                 int32_t ntree, int32_t mtry, int64_t iseed, int32_t min_node_size,
-                 int64_t max_nodes, int32_t nthreads)
+                 int32_t first_tree, int32_t ntree, int32_t mtry, int64_t iseed,
+                 int32_t min_node_size, int64_t max_nodes, int32_t nthreads)
 {
     Problem P{values, labels, col_cat, col_levels, n, p, n_classes, mtry,
               min_node_size, max_nodes};
@@ -335,13 +338,14 @@ void* rfxt_train(const double* values, int64_t n, int32_t p, const int32_t* labe
         TreeOut& T = F->trees[t];
         T.inbag.assign(n, 0);
         uint64_t st[2];
-        rfx_pcg32_make(iseed + t, RFX_SEQ_TREE, st);
+        const int64_t tree_seed = iseed + first_tree + t;
+        rfx_pcg32_make(tree_seed, RFX_SEQ_TREE, st);
         for (int64_t d = 0; d < n; d++) T.inbag[rfx_pcg32_bounded(st, (uint32_t)n)] += 1;
-        grow(P, iseed + t, T);
+        grow(P, tree_seed, T);
     }
     for (int32_t t = 0; t < ntree; t++) {
         if (F->trees[t].error) {
-            g_err = "tree " + std::to_string(t) + ": exceeded max_nodes=" +
+            g_err = "tree " + std::to_string(first_tree + t) + ": exceeded max_nodes=" +
                     std::to_string(max_nodes);
             delete F;
             return nullptr;

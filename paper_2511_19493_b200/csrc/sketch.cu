@@ -188,16 +188,16 @@ int gram_parts(int64_t n)
 }
 
 __global__ void __launch_bounds__(GRAM_THREADS)
-gram_partial_kernel(const double* __restrict__ A, const double* __restrict__ Bm, int64_t n, int ka,
-                    int kb, int64_t rows_per_part, double* __restrict__ parts)
+gram_partial_kernel(const double* __restrict__ A, int lda, const double* __restrict__ Bm, int ldb,
+                    int64_t n, int ka, int kb, int64_t rows_per_part, double* __restrict__ parts)
 {
     extern __shared__ double gsm[];
     double* As = gsm;                       // GRAM_ROWS x ka
     double* Bs = gsm + GRAM_ROWS * ka;      // GRAM_ROWS x kb
     const int64_t r0 = blockIdx.x * rows_per_part;
-    const int64_t r1 = min(n, r0 + rows_per_part);
+    const int64_t r1 = min64(n, r0 + rows_per_part);
     const int E = ka * kb;
-    constexpr int MAXE = 64;  // entries per thread (ka*kb <= 64*256)
+    constexpr int MAXE = 64;  // entries per thread (ka*kb <= 64*256 per launch)
     double acc[MAXE];
 #pragma unroll
     for (int q = 0; q < MAXE; q++) acc[q] = 0.0;
@@ -205,11 +205,11 @@ gram_partial_kernel(const double* __restrict__ A, const double* __restrict__ Bm,
         const int m = (int)min64(GRAM_ROWS, r1 - base);
         for (int e = threadIdx.x; e < GRAM_ROWS * ka; e += GRAM_THREADS) {
             const int r = e / ka;
-            As[e] = r < m ? A[(base + r) * ka + e % ka] : 0.0;
+            As[e] = r < m ? A[(base + r) * lda + e % ka] : 0.0;
         }
         for (int e = threadIdx.x; e < GRAM_ROWS * kb; e += GRAM_THREADS) {
             const int r = e / kb;
-            Bs[e] = r < m ? Bm[(base + r) * kb + e % kb] : 0.0;
+            Bs[e] = r < m ? Bm[(base + r) * ldb + e % kb] : 0.0;
         }
         __syncthreads();
 #pragma unroll
@@ -232,14 +232,16 @@ gram_partial_kernel(const double* __restrict__ A, const double* __restrict__ Bm,
     }
 }
 
-__global__ void gram_final_kernel(const double* __restrict__ parts, int nparts, int E,
-                                  double* __restrict__ C)
+// C[:, c0:c0+kb] (row stride ldc) = sum over parts, fixed order
+__global__ void gram_final_kernel(const double* __restrict__ parts, int nparts, int ka, int kb,
+                                  double* __restrict__ C, int ldc, int c0)
 {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int E = ka * kb;
     if (e >= E) return;
     double s = 0.0;
     for (int q = 0; q < nparts; q++) s += parts[(int64_t)q * E + e];
-    C[e] = s;
+    C[(e / kb) * ldc + c0 + e % kb] = s;
 }
 
 // --------------------------------------------------------- small matmul
@@ -327,21 +329,29 @@ extern "C" int rfxc_gram_parts(int64_t n) { return gram_parts(n); }
 extern "C" int rfxc_gram(const double* d_A, const double* d_B, int64_t n, int32_t ka, int32_t kb,
                          double* d_partials, double* d_C, void* stream)
 {
-    if (n < 1 || ka < 1 || kb < 1 || (int64_t)ka * kb > 64 * GRAM_THREADS)
+    // d_partials must hold rfxc_gram_parts(n) * ka * kb doubles
+    if (n < 1 || ka < 1 || kb < 1 || ka > 64 * GRAM_THREADS)
         return fail(RFXC_EDATA, "gram: bad shape ka=%d kb=%d", ka, kb);
     cudaStream_t st = as_stream(stream);
     const int parts = gram_parts(n);
     const int64_t rpp = ceil_div(n, parts);
-    const size_t smem = (size_t)GRAM_ROWS * (ka + kb) * 8;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(gram_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    gram_partial_kernel<<<parts, GRAM_THREADS, smem, st>>>(d_A, d_B, n, ka, kb, rpp, d_partials);
-    int rc = check_launch("gram_partial");
-    if (rc) return rc;
-    const int E = ka * kb;
-    gram_final_kernel<<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(d_partials, parts, E, d_C);
-    return check_launch("gram_final");
+    const int kbc = std::max(1, std::min<int>(kb, 64 * GRAM_THREADS / ka));  // columns per launch
+    for (int c0 = 0; c0 < kb; c0 += kbc) {
+        const int w = std::min(kbc, kb - c0);
+        const size_t smem = (size_t)GRAM_ROWS * (ka + w) * 8;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(gram_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        gram_partial_kernel<<<parts, GRAM_THREADS, smem, st>>>(d_A, ka, d_B + c0, kb, n, ka, w, rpp,
+                                                               d_partials);
+        int rc = check_launch("gram_partial");
+        if (rc) return rc;
+        gram_final_kernel<<<(unsigned)ceil_div((int64_t)ka * w, 256), 256, 0, st>>>(
+            d_partials, parts, ka, w, d_C, kb, c0);
+        rc = check_launch("gram_final");
+        if (rc) return rc;
+    }
+    return RFXC_OK;
 }
 
 extern "C" int rfxc_matmul_small(const double* d_Y, int64_t n, int32_t ka, const double* d_M,

@@ -15,10 +15,13 @@ only when a caller reads them.
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 
 from . import _lib
 from .errors import DataError
+from .profiling import region
 
 
 def _torch():
@@ -141,7 +144,9 @@ class DeviceValues:
         vals = np.asfortranarray(values, dtype=np.float64)
         self.n, self.p = vals.shape
         # F-order (n, p) is exactly (p, n) row-major
-        self.f64 = torch.from_numpy(vals.T).to(dev)
+        with warnings.catch_warnings():  # read-only Dataset.values: torch only reads it
+            warnings.simplefilter("ignore", UserWarning)
+            self.f64 = torch.from_numpy(vals.T).to(dev)
         self.f32 = torch.empty((self.p, self.n), dtype=torch.float32, device=dev)
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
         _lib.call("rfxc_values_to_f32", _lib.ptr(self.f64), self.n * self.p,
@@ -186,9 +191,10 @@ class DeviceMembership:
             seg = torch.empty(self.total_leaves + 1, dtype=torch.int64, device=dev)
             maxl = int(self.leaf_counts.max())
             scratch = torch.empty(max(self.total_leaves, 1), dtype=torch.int32, device=dev)
-            _lib.call("rfxc_bucket", _lib.ptr(self.codes_tm), self.n, self.Bl,
-                      _lib.ptr(self.leaf_base), maxl, _lib.ptr(perm), _lib.ptr(seg),
-                      _lib.ptr(scratch), _lib.stream_handle())
+            with region("bucket"):
+                _lib.call("rfxc_bucket", _lib.ptr(self.codes_tm), self.n, self.Bl,
+                          _lib.ptr(self.leaf_base), maxl, _lib.ptr(perm), _lib.ptr(seg),
+                          _lib.ptr(scratch), _lib.stream_handle())
             self._perm, self._seg = perm, seg
         return self._perm, self._seg
 
@@ -218,8 +224,10 @@ def traverse(dforest: DeviceForest, dvalues: DeviceValues) -> DeviceMembership:
     n, Bl = dvalues.n, dforest.ntree
     dev = vals.device
     tm = torch.empty((Bl, n), dtype=torch.int32, device=dev)
-    _lib.call("rfxc_leaf_codes", _lib.ptr(dforest.packed(layout)), _lib.ptr(dforest.node_off),
-              layout, dvalues.p, 0, Bl, _lib.ptr(vals), n, _lib.ptr(tm), _lib.stream_handle())
+    nodes = dforest.packed(layout)
+    with region("leaf_codes"):
+        _lib.call("rfxc_leaf_codes", _lib.ptr(nodes), _lib.ptr(dforest.node_off), layout,
+                  dvalues.p, 0, Bl, _lib.ptr(vals), n, _lib.ptr(tm), _lib.stream_handle())
     nb = torch.empty((n, Bl), dtype=torch.int32, device=dev)
     _lib.call("rfxc_transpose_i32", _lib.ptr(tm), Bl, n, _lib.ptr(nb), _lib.stream_handle())
     return nb, tm, layout

@@ -53,6 +53,18 @@ def row_shard(n: int, rank: int, world: int) -> tuple[int, int]:
     return boundary(rank), boundary(rank + 1)
 
 
+def all_reduce_int(value: int, group=None) -> int:
+    """Sum of a Python int over the ranks (device tensor under NCCL)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return int(value)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([int(value)], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return int(t.item())
+
+
 def all_reduce_sum(tensor, group=None):
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:

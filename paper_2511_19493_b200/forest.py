@@ -118,7 +118,7 @@ def _tlib():
         L = ctypes.CDLL(_lib.TRAIN_LIB_PATH)
         P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         L.rfxt_train.restype = P
-        L.rfxt_train.argtypes = [P, I64, I32, P, I32, P, P, I32, I32, I64, I32, I64, I32]
+        L.rfxt_train.argtypes = [P, I64, I32, P, I32, P, P, I32, I32, I32, I64, I32, I64, I32]
         L.rfxt_last_error.restype = ctypes.c_char_p
         L.rfxt_node_counts.argtypes = [P, P]
         L.rfxt_copy.argtypes = [P] * 13
@@ -131,15 +131,25 @@ def _p(a):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
-def train(dataset: Dataset, config: TrainConfig, nthreads: int = 0) -> Forest:
-    """Grow the forest exactly as rfx.train does (forest.py:262-302)."""
+def train(dataset: Dataset, config: TrainConfig, nthreads: int = 0,
+          trees: tuple | None = None) -> Forest:
+    """Grow the forest exactly as rfx.train does (forest.py:262-302).
+
+    ``trees=(lo, hi)`` grows only that tree range of the ``config.ntree``
+    forest (tree t is seeded by iseed + t, so a shard's trees are identical to
+    the whole forest's); the returned Forest then holds hi - lo trees and its
+    OOB votes cover those trees only."""
     cfg = config.resolved(dataset.n, dataset.p)
     col_cat, col_levels = column_arrays(dataset.columns)
-    n, p, C, B = dataset.n, dataset.p, dataset.class_count, cfg.ntree
+    n, p, C = dataset.n, dataset.p, dataset.class_count
+    lo, hi = (0, cfg.ntree) if trees is None else (int(trees[0]), int(trees[1]))
+    if not 0 <= lo < hi <= cfg.ntree:
+        raise DataError(f"tree range {trees} outside [0, {cfg.ntree})")
+    B = hi - lo
     vals = np.asfortranarray(dataset.values, dtype=np.float64)
     labels = np.ascontiguousarray(dataset.labels, dtype=np.int32)
     L = _tlib()
-    h = L.rfxt_train(_p(vals), n, p, _p(labels), C, _p(col_cat), _p(col_levels), B,
+    h = L.rfxt_train(_p(vals), n, p, _p(labels), C, _p(col_cat), _p(col_levels), lo, B,
                      cfg.mtry, cfg.iseed, cfg.min_node_size, cfg.max_nodes, nthreads)
     if not h:
         raise RfxError(L.rfxt_last_error().decode())
@@ -165,6 +175,7 @@ def train(dataset: Dataset, config: TrainConfig, nthreads: int = 0) -> Forest:
     finally:
         L.rfxt_free(h)
     off = np.concatenate([[0], np.cumsum(counts)])
+    shard = None if (lo, hi) == (0, cfg.ntree) else (lo, hi, cfg.ntree)
     trees = []
     for b in range(B):
         s, e = int(off[b]), int(off[b + 1])
@@ -172,9 +183,10 @@ def train(dataset: Dataset, config: TrainConfig, nthreads: int = 0) -> Forest:
                           cat_mask[s:e].copy(), left[s:e].copy(), right[s:e].copy(),
                           node_class[s:e].copy(), class_pops[s * C:e * C].reshape(e - s, C),
                           node_raw[s:e].copy(), node_weight[s:e].copy(), col_cat))
-    return Forest(trees=tuple(trees), bootstrap=BootstrapRecord(inbag), config=cfg, n=n,
-                  p=p, class_count=C, col_cat=col_cat, col_levels=col_levels,
-                  oob_votes=votes)
+    f = Forest(trees=tuple(trees), bootstrap=BootstrapRecord(inbag), config=cfg, n=n,
+               p=p, class_count=C, col_cat=col_cat, col_levels=col_levels, oob_votes=votes)
+    f.tree_range = shard  # (lo, hi, B_total) for a shard-grown forest, else None
+    return f
 
 
 # --------------------------------------------------------------- RFX1 format

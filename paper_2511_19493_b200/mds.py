@@ -16,6 +16,7 @@ import numpy as np
 
 from . import _lib
 from .errors import DataError, RfxError
+from .profiling import region
 from .proximity import FullTriangle, LowRankQuantized, TriBlock
 
 logger = logging.getLogger(__name__)
@@ -118,15 +119,17 @@ def mds_lowrank_device(lowrank: LowRankQuantized, config: PowerIterConfig | None
     (coords (n, k), info (k, 4), k_used (1,))."""
     import torch
     cfg = config or PowerIterConfig()
-    dq = lowrank.dequantized_device()
+    dq = lowrank.dq if hasattr(lowrank, "dq") else lowrank.dequantized_device()
     n, r = dq.shape
     dev = dq.device
     coords = torch.empty((n, cfg.k), dtype=torch.float64, device=dev)
     info = torch.empty((cfg.k, 4), dtype=torch.float64, device=dev)
     kused = torch.empty(1, dtype=torch.int32, device=dev)
-    _lib.call("rfxc_mds_power", _lib.ptr(dq), n, r, float(lowrank.pmax), cfg.k,
-              cfg.max_iterations, float(cfg.tol), cfg.seed, _lib.ptr(coords), _lib.ptr(info),
-              _lib.ptr(kused), _lib.ptr(_work(n, r, cfg.k, dev)), _lib.stream_handle())
+    work = _work(n, r, cfg.k, dev)
+    with region("mds_power"):
+        _lib.call("rfxc_mds_power", _lib.ptr(dq), n, r, float(lowrank.pmax), cfg.k,
+                  cfg.max_iterations, float(cfg.tol), cfg.seed, _lib.ptr(coords),
+                  _lib.ptr(info), _lib.ptr(kused), _lib.ptr(work), _lib.stream_handle())
     return coords, info, kused
 
 

@@ -27,6 +27,7 @@ import numpy as np
 from . import _lib
 from .device import DeviceForest, DeviceMembership, DeviceValues, traverse
 from .errors import BudgetError, DataError, RfxError
+from .profiling import region
 from .quantize import (BYTES_PER_ELEMENT, MODES, QuantFactor, dequantize,
                        device_dequantize, factor_quantize, to_host)
 
@@ -100,7 +101,13 @@ class LeafMembership:
 
     @property
     def total_leaves(self) -> int:
-        return int(self.leaf_counts.sum())
+        """Leaves over the whole forest (all-reduced over the ranks when this
+        membership is a tree shard)."""
+        local = int(self.leaf_counts.sum())
+        if self._dev is None or not self._dev.is_shard:
+            return local
+        from .distributed import all_reduce_int
+        return all_reduce_int(local)
 
     @property
     def tree_range(self):
@@ -132,23 +139,28 @@ class LeafMembership:
 def leaf_membership(forest, dataset, trees: tuple | None = None) -> LeafMembership:
     """Classify every sample down every tree on the GPU (proximity.py:100-116).
 
-    ``trees=(lo, hi)`` restricts the work to a tree shard (multi-GPU)."""
+    Tree shards (multi-GPU): ``trees=(lo, hi)`` restricts the work to that
+    range of ``forest``; a forest grown as a shard (``train(...,
+    trees=(lo, hi))``, carrying ``tree_range``) is a shard by itself.  The
+    membership of a shard keeps the forest-wide tree count B (the 1/B of
+    every proximity) and its own trees' leaf counts."""
     if forest.n != dataset.n or forest.p != dataset.p:
         raise DataError("forest and dataset shapes disagree")
-    B = forest.ntree
-    lo, hi = (0, B) if trees is None else (int(trees[0]), int(trees[1]))
-    if not 0 <= lo < hi <= B:
-        raise DataError(f"tree range {trees} outside [0, {B})")
-    dforest = DeviceForest(forest, lo, hi)
+    grown = getattr(forest, "tree_range", None)
+    if grown is not None:
+        lo, hi, B = grown
+        local = (0, forest.ntree)
+    else:
+        B = forest.ntree
+        lo, hi = (0, B) if trees is None else (int(trees[0]), int(trees[1]))
+        if not 0 <= lo < hi <= B:
+            raise DataError(f"tree range {trees} outside [0, {B})")
+        local = (lo, hi)
+    dforest = DeviceForest(forest, *local)
     dvals = DeviceValues(dataset.values)
     nb, tm, _ = traverse(dforest, dvals)
     dev = DeviceMembership(nb, tm, dforest.leaf_counts, lo, hi, B)
-    if lo == 0 and hi == B:
-        lc = dforest.leaf_counts
-    else:
-        lc = np.array([int((np.asarray(t.status) == 1).sum()) for t in forest.trees],
-                      dtype=np.int32)
-    return LeafMembership(leaf_counts=lc, _dev=dev)
+    return LeafMembership(leaf_counts=dforest.leaf_counts, _dev=dev)
 
 
 # ------------------------------------------------------------- full triangle
@@ -472,11 +484,14 @@ class _Sketch:
         import torch
         d = self.d
         Y = torch.empty((d.n, kk), dtype=torch.float64, device=X32.device)
-        _lib.call("rfxc_leaf_sums", _lib.ptr(self.perm), _lib.ptr(self.seg), 0, d.total_leaves,
-                  _lib.ptr(X32), kk, self.ld, _lib.ptr(self.S), _lib.stream_handle())
-        _lib.call("rfxc_leaf_gather", _lib.ptr(d.codes_nb), d.n, d.Bl, _lib.ptr(d.leaf_base),
-                  _lib.ptr(self.S), kk, self.ld, 1.0 / d.B, 0, _lib.ptr(Y),
-                  _lib.stream_handle())
+        with region("leaf_sums"):
+            _lib.call("rfxc_leaf_sums", _lib.ptr(self.perm), _lib.ptr(self.seg), 0,
+                      d.total_leaves, _lib.ptr(X32), kk, self.ld, _lib.ptr(self.S),
+                      _lib.stream_handle())
+        with region("leaf_gather"):
+            _lib.call("rfxc_leaf_gather", _lib.ptr(d.codes_nb), d.n, d.Bl, _lib.ptr(d.leaf_base),
+                      _lib.ptr(self.S), kk, self.ld, 1.0 / d.B, 0, _lib.ptr(Y),
+                      _lib.stream_handle())
         if d.is_shard and reduce:
             import torch.distributed as dist
             dist.all_reduce(Y, op=dist.ReduceOp.SUM, group=self.group)
@@ -514,6 +529,11 @@ def orthonormalize(Y, ld: int):
     skinny reduction), host k x k eigh / Cholesky, Q = Y M (device).
     Directions below the f64 noise floor of G are dropped (k' <= k).
     Returns (Q f64 (n, k'), Q32 f32 (n, ld'))."""
+    with region("orthonormalize"):
+        return _orthonormalize(Y, ld)
+
+
+def _orthonormalize(Y, ld: int):
     G = _gram(Y, Y)
     lam, V = np.linalg.eigh(0.5 * (G + G.T))
     top = lam.max() if lam.size else 0.0
@@ -532,11 +552,9 @@ def orthonormalize(Y, ld: int):
     return _times(Q1, Rinv, ld)
 
 
-def lowrank_proximity(membership: LeafMembership, rank: int, mode: str = "i8",
-                      seed: int = 0, group=None) -> LowRankQuantized:
-    """Randomised symmetric rank-r factorisation of P = M M^T followed by
-    quantisation (proximity.py:367-420), with P applied implicitly on the
-    GPU (K4) and never materialised."""
+def lowrank_device(membership: LeafMembership, rank: int, mode: str = "i8", seed: int = 0,
+                   group=None) -> "DeviceLowRank":
+    """The device pipeline behind lowrank_proximity (results stay in HBM)."""
     import torch
     if mode not in MODES:
         raise DataError(f"unknown quantization mode {mode!r}")
@@ -572,16 +590,48 @@ def lowrank_proximity(membership: LeafMembership, rank: int, mode: str = "i8",
     Wr = W[:, order] * np.sqrt(lam)[None, :]
     if Wr.shape[1] < r:  # numerically rank-deficient: zero factor columns
         Wr = np.pad(Wr, ((0, 0), (0, r - Wr.shape[1])))
-    data, scales = factor_quantize(Q, Wr, mode)
+    with region("factor_quantize"):
+        data, scales = factor_quantize(Q, Wr, mode)
     dq = device_dequantize(data, scales, n, r, mode)
     parts = torch.empty(_lib.load().rfxc_gram_parts(n) + 1, dtype=torch.float64, device=dev)
     pm = torch.empty(1, dtype=torch.float64, device=dev)
-    _lib.call("rfxc_pmax", _lib.ptr(dq), n, r, seed, _lib.ptr(parts), _lib.ptr(pm),
-              _lib.stream_handle())
-    qf = to_host(mode, (n, r), data, scales)
-    return LowRankQuantized(n=n, rank=r, mode=mode, factor=qf, pmax=float(pm.item()),
-                            tree_count=membership.tree_count, rank_degraded=degraded,
-                            _dq_dev=dq)
+    with region("pmax"):
+        _lib.call("rfxc_pmax", _lib.ptr(dq), n, r, seed, _lib.ptr(parts), _lib.ptr(pm),
+                  _lib.stream_handle())
+    return DeviceLowRank(n=n, rank=r, mode=mode, data=data, scales=scales, dq=dq,
+                         pmax=float(pm.item()), tree_count=membership.tree_count,
+                         degraded=degraded)
+
+
+@dataclass
+class DeviceLowRank:
+    """Device-resident result of the low-rank pipeline (factor codes, scales,
+    dequantised factor) before any host copy."""
+
+    n: int
+    rank: int
+    mode: str
+    data: object
+    scales: object
+    dq: object
+    pmax: float
+    tree_count: int
+    degraded: bool
+
+    def to_host(self) -> LowRankQuantized:
+        qf = to_host(self.mode, (self.n, self.rank), self.data, self.scales)
+        return LowRankQuantized(n=self.n, rank=self.rank, mode=self.mode, factor=qf,
+                                pmax=self.pmax, tree_count=self.tree_count,
+                                rank_degraded=self.degraded, _dq_dev=self.dq)
+
+
+def lowrank_proximity(membership: LeafMembership, rank: int, mode: str = "i8",
+                      seed: int = 0, group=None) -> LowRankQuantized:
+    """Randomised symmetric rank-r factorisation of P = M M^T followed by
+    quantisation (proximity.py:367-420), with P applied implicitly on the
+    GPU (K4) and never materialised.  ``group``: torch.distributed group of
+    the tree shards when ``membership`` is a shard."""
+    return lowrank_device(membership, rank, mode, seed, group).to_host()
 
 
 # ------------------------------------------------------------------ accessors
