@@ -81,6 +81,27 @@ int rfxc_forest_pack(const int8_t* d_status, const int32_t* d_split_var,
                      int32_t p, int32_t layout, void* d_nodes,
                      int32_t* d_leaf_counts, void* stream);
 
+/* Host-side packing (upload boundary, csrc/host/host_pack.cpp): the same
+ * records as rfxc_forest_pack, built on the host from PER-TREE host arrays
+ * (h pointer tables of length B: the reference's Tree fields, dtypes int8 /
+ * int32 / f64 / int64 / int32 / int32) into a caller (pinned) buffer, so only
+ * 8 or 16 B/node cross PCIe.  Trees with right != left + 1 are relaid out
+ * breadth-first, keeping the reference leaf ordinals.  Also fills
+ * h_node_off (B+1) and h_leaf_counts (B).  Synchronous, multi-threaded
+ * (nthreads <= 0: all cores). */
+int rfxc_forest_pack_host(const void* const* h_status, const void* const* h_split_var,
+                          const void* const* h_threshold, const void* const* h_cat_mask,
+                          const void* const* h_left, const void* const* h_right,
+                          const int64_t* h_node_counts, int32_t B,
+                          const uint8_t* h_col_cat, int32_t p, int32_t layout,
+                          void* h_nodes, int64_t* h_node_off, int32_t* h_leaf_counts,
+                          int32_t nthreads);
+
+/* Host f64 -> f32 copy of the values with an exactness verdict
+ * (*h_exact = 1 when every value is f32-representable). */
+int rfxc_values_to_f32_host(const double* h_values, int64_t count, float* h_out,
+                            int32_t* h_exact, int32_t nthreads);
+
 /* K1 — leaf code of every sample in trees [tree_lo, tree_hi) into
  * d_codes_tm ((tree_hi - tree_lo) x n).  Replaces descend/descend_all
  * (_kernels.py:333-374) driven by leaf_membership (proximity.py:100-116).
@@ -206,9 +227,13 @@ int rfxc_pmax(const double* d_dq, int64_t n, int32_t r, int64_t seed,
  * matvec is gram_matvec (mds.py:161-181) on the UNclamped P = dq dq^T.
  * Outputs: d_coords (n, k) row-major f64 = sqrt(lambda) * sign_fixed v
  * (mds.py:257-261); d_info: per component {lambda, iterations, residual,
- * converged} as 4 f64; *d_k_used (int32).  d_work: rfxc_mds_work_bytes(). */
+ * converged} as 4 f64; *d_k_used (int32).  d_work: rfxc_mds_work_bytes().
+ * d_codes / d_scales (nullable): the INT8 factor; when given, large-n runs
+ * keep the factor slice of every CTA resident in shared memory as int8
+ * codes (code * scale is bit-identical to d_dq). */
 int64_t rfxc_mds_work_bytes(int64_t n, int32_t r, int32_t k);
-int rfxc_mds_power(const double* d_dq, int64_t n, int32_t r, double pmax,
+int rfxc_mds_power(const double* d_dq, const int8_t* d_codes, const double* d_scales,
+                   int64_t n, int32_t r, double pmax,
                    int32_t k, int32_t max_iterations, double tol, int64_t seed,
                    double* d_coords, double* d_info, int32_t* d_k_used,
                    void* d_work, void* stream);

@@ -36,6 +36,9 @@ SIGNATURES = {
     "rfxc_device_info": (ctypes.c_int, [ctypes.c_int, P, P, P]),
     "rfxc_values_to_f32": (ctypes.c_int, [P, I64, P, P, P]),
     "rfxc_forest_pack": (ctypes.c_int, [P, P, P, P, P, P, P, I32, I64, P, I32, I32, P, P, P]),
+    "rfxc_forest_pack_host": (ctypes.c_int, [P, P, P, P, P, P, P, I32, P, I32, I32, P, P, P,
+                                             I32]),
+    "rfxc_values_to_f32_host": (ctypes.c_int, [P, I64, P, P, I32]),
     "rfxc_leaf_codes": (ctypes.c_int, [P, P, I32, I32, I32, I32, P, I64, P, P]),
     "rfxc_transpose_i32": (ctypes.c_int, [P, I64, I64, P, P]),
     "rfxc_bucket": (ctypes.c_int, [P, I64, I32, P, I32, P, P, P, P]),
@@ -55,7 +58,8 @@ SIGNATURES = {
     "rfxc_dequantize": (ctypes.c_int, [P, P, I64, I32, I32, P, P]),
     "rfxc_pmax": (ctypes.c_int, [P, I64, I32, I64, P, P, P]),
     "rfxc_mds_work_bytes": (I64, [I64, I32, I32]),
-    "rfxc_mds_power": (ctypes.c_int, [P, I64, I32, F64, I32, I32, F64, I64, P, P, P, P, P]),
+    "rfxc_mds_power": (ctypes.c_int, [P, P, P, I64, I32, F64, I32, I32, F64, I64, P, P, P, P,
+                                      P]),
     "rfxc_gram_matvec": (ctypes.c_int, [P, I64, I32, F64, P, P, P, P]),
 }
 
@@ -110,7 +114,7 @@ def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
     launch_count += LAUNCHES.get(name, 0)
     if name == "rfxc_mds_power":
-        launch_count += int(args[4])  # start-vector normals, one per component
+        launch_count += int(args[6])  # start-vector normals, one per component
 
 
 def ptr(t) -> ctypes.c_void_p:

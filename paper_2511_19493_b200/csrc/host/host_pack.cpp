@@ -1,0 +1,207 @@
+// host_pack.cpp — host side of the upload boundary (part of librfxc.so).
+//
+// The drop-in API receives the forest as per-tree host arrays (forest.py:67-99,
+// _kernels.py:7-17) and the dataset as a column-major f64 matrix
+// (dataset.py:59-71).  Instead of shipping ~25 B/node of raw arrays over PCIe
+// and repacking on the device, these functions pack the traversal records
+// (8 B/node f32 layout, 16 B/node f64 layout — same encoding as the device
+// packer in forest.cu) and the f32 feature copy directly into caller-owned
+// (pinned) host buffers with one thread per core, so only the packed bytes
+// cross the bus.  Trees whose right child is not left + 1 (hand-built trees;
+// trained trees always satisfy it, _kernels.py:313-317) are relaid out
+// breadth-first here, keeping the reference's leaf ordinals.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../../include/rfxc.h"
+
+namespace rfxc {
+std::string& last_error();
+}
+
+namespace {
+
+int feature_bits(int p)
+{
+    int fb = 1;
+    while ((1 << fb) < p) fb++;
+    return fb;
+}
+
+// f64 -> f32 rounded toward -inf (exact compare for f32-representable x)
+inline float round_down_f32(double t)
+{
+    float f = (float)t;
+    if ((double)f > t) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+
+template <class F>
+void parallel_for(int64_t count, int nthreads, F&& fn)
+{
+    if (nthreads <= 1 || count < 2) {
+        for (int64_t i = 0; i < count; i++) fn(i);
+        return;
+    }
+    std::vector<std::thread> ts;
+    std::atomic<int64_t> next{0};
+    for (int t = 0; t < nthreads; t++)
+        ts.emplace_back([&] {
+            for (int64_t i; (i = next.fetch_add(1)) < count;) fn(i);
+        });
+    for (auto& t : ts) t.join();
+}
+
+int hw_threads(int requested)
+{
+    if (requested > 0) return requested;
+    unsigned h = std::thread::hardware_concurrency();
+    return h ? (int)h : 1;
+}
+
+}  // namespace
+
+extern "C" int rfxc_forest_pack_host(const void* const* status, const void* const* split_var,
+                                     const void* const* threshold, const void* const* cat_mask,
+                                     const void* const* left, const void* const* right,
+                                     const int64_t* node_counts, int32_t B,
+                                     const uint8_t* col_cat, int32_t p, int32_t layout,
+                                     void* h_nodes, int64_t* h_node_off,
+                                     int32_t* h_leaf_counts, int32_t nthreads)
+{
+    if (B < 1 || p < 1) {
+        rfxc::last_error() = "forest_pack_host: bad shape";
+        return RFXC_EDATA;
+    }
+    h_node_off[0] = 0;
+    for (int b = 0; b < B; b++) h_node_off[b + 1] = h_node_off[b] + node_counts[b];
+    const int fb = feature_bits(p);
+    const int64_t max_left = layout == RFXC_NODES_F32 ? (int64_t(1) << (31 - fb)) : INT32_MAX;
+    std::vector<std::string> errs(B);
+    parallel_for(B, hw_threads(nthreads), [&](int64_t b) {
+        const int64_t nc = node_counts[b];
+        const int8_t* st = static_cast<const int8_t*>(status[b]);
+        const int32_t* sv = static_cast<const int32_t*>(split_var[b]);
+        const double* th = static_cast<const double*>(threshold[b]);
+        const int64_t* cm = static_cast<const int64_t*>(cat_mask[b]);
+        const int32_t* lf = static_cast<const int32_t*>(left[b]);
+        const int32_t* rt = static_cast<const int32_t*>(right[b]);
+        // order[new] = old node id; identity when siblings are adjacent
+        std::vector<int64_t> order;
+        bool adjacent = true;
+        for (int64_t t = 0; t < nc && adjacent; t++)
+            if (st[t] == 0 && rt[t] != lf[t] + 1) adjacent = false;
+        std::vector<int32_t> code(nc, -1);
+        int32_t nleaf = 0;
+        for (int64_t t = 0; t < nc; t++)
+            if (st[t] == 1) code[t] = nleaf++;
+        h_leaf_counts[b] = nleaf;
+        std::vector<int64_t> newid;
+        if (!adjacent) {
+            order.reserve(nc);
+            newid.assign(nc, -1);
+            order.push_back(0);
+            newid[0] = 0;
+            for (size_t q = 0; q < order.size(); q++) {
+                const int64_t o = order[q];
+                if (st[o] == 0) {
+                    for (int64_t ch : {(int64_t)lf[o], (int64_t)rt[o]}) {
+                        if (ch <= 0 || ch >= nc || newid[ch] >= 0) {
+                            errs[b] = "tree " + std::to_string(b) + ": malformed children";
+                            return;
+                        }
+                        newid[ch] = (int64_t)order.size();
+                        order.push_back(ch);
+                    }
+                }
+            }
+            if ((int64_t)order.size() != nc) {
+                errs[b] = "tree " + std::to_string(b) + ": unreachable nodes";
+                return;
+            }
+        }
+        const int64_t base = h_node_off[b];
+        for (int64_t t = 0; t < nc; t++) {
+            const int64_t o = adjacent ? t : order[t];
+            const bool leaf = st[o] == 1;
+            const int64_t l = leaf ? 0 : (adjacent ? lf[o] : newid[lf[o]]);
+            if (!leaf && (l < 1 || l >= max_left)) {
+                errs[b] = "tree " + std::to_string(b) + ": child id out of range for layout";
+                return;
+            }
+            const int f = leaf ? 0 : sv[o];
+            if (!leaf && (f < 0 || f >= p)) {
+                errs[b] = "tree " + std::to_string(b) + ": split_var out of range";
+                return;
+            }
+            const bool cat = !leaf && col_cat[f] == 1;
+            if (layout == RFXC_NODES_F32) {
+                uint32_t x, y;
+                if (leaf) {
+                    x = (uint32_t)code[o];
+                    y = 0u;
+                } else {
+                    if (cat) {
+                        x = (uint32_t)(cm[o] & 0xffffffffLL);
+                    } else {
+                        float fr = round_down_f32(th[o]);
+                        std::memcpy(&x, &fr, 4);
+                    }
+                    y = ((uint32_t)l << (fb + 1)) | ((uint32_t)cat << fb) | (uint32_t)f;
+                }
+                uint32_t* rec = static_cast<uint32_t*>(h_nodes) + 2 * (base + t);
+                rec[0] = x;
+                rec[1] = y;
+            } else {
+                int32_t* rec = static_cast<int32_t*>(h_nodes) + 4 * (base + t);
+                if (leaf) {
+                    rec[0] = rec[1] = 0;
+                    rec[2] = -1;
+                    rec[3] = code[o];
+                } else {
+                    int64_t bits;
+                    if (cat) bits = cm[o];
+                    else std::memcpy(&bits, &th[o], 8);
+                    rec[0] = (int32_t)(bits & 0xffffffffLL);
+                    rec[1] = (int32_t)(bits >> 32);
+                    rec[2] = f | ((int)cat << 30);
+                    rec[3] = (int32_t)l;
+                }
+            }
+        }
+    });
+    for (int b = 0; b < B; b++)
+        if (!errs[b].empty()) {
+            rfxc::last_error() = errs[b];
+            return RFXC_EDATA;
+        }
+    return RFXC_OK;
+}
+
+extern "C" int rfxc_values_to_f32_host(const double* h_values, int64_t count, float* h_out,
+                                       int32_t* exact, int32_t nthreads)
+{
+    const int T = hw_threads(nthreads);
+    const int64_t chunk = (count + T - 1) / T;
+    std::vector<int> bad(T, 0);
+    parallel_for(T, T, [&](int64_t t) {
+        const int64_t lo = t * chunk, hi = std::min(count, lo + chunk);
+        int b = 0;
+        for (int64_t i = lo; i < hi; i++) {
+            const float f = (float)h_values[i];
+            h_out[i] = f;
+            b |= ((double)f != h_values[i]);
+        }
+        bad[t] = b;
+    });
+    int any = 0;
+    for (int b : bad) any |= b;
+    *exact = !any;
+    return RFXC_OK;
+}

@@ -4,21 +4,26 @@
 // mds_lowrank (mds.py:184-268): for each of k eigenpairs, start from
 // Pcg32(seed + c, SEQ_POWER).normals(n), orthogonalise against the found
 // vectors, iterate w = G v - sum_f lambda_f (v_f.v) v_f, project out the
-// found vectors (sequential Gram-Schmidt), lambda = v.w, v <- w/|w| with the
-// sign aligned to the previous iterate, stop when max|v_new - v| < tol or at
-// the iteration cap; relative residual |G v - lambda v| / |lambda|; stop at
-// lambda <= 0.  Coordinates sqrt(lambda) * v with the largest-|component|
-// positive (mds.py:83-86, :257-261).
+// found vectors, lambda = v.w, v <- w/|w| with the sign aligned to the
+// previous iterate, stop when max|v_new - v| < tol or at the iteration cap;
+// relative residual |G v - lambda v| / |lambda|; stop at lambda <= 0.
+// Coordinates sqrt(lambda) * v, largest-|component| positive
+// (mds.py:83-86, :257-261).
 //
-// G v = -1/2 H D2 H v with D2 u = pmax^2 (sum u) 1 - 2 pmax P u + (P o P) u and
-// the UNclamped P = Q Q^T (mds.py:177-179).  (P o P) u is evaluated as
-// q_i^T S q_i with S = Q^T diag(u) Q (r x r) — the Khatri-Rao identity of
-// mds.py:147-152 without the n x r^2 expansion.
+// G v = -1/2 H D2 H v with D2 u = pmax^2 (sum u) 1 - 2 pmax P u + (P o P) u on
+// the UNclamped P = Q Q^T (mds.py:177-179).  With Q' = [Q | 1] the single
+// reduction S' = Q'^T diag(u) Q' holds S = Q^T diag(u) Q (so that
+// (P o P)u_i = q_i^T S q_i — the Khatri-Rao identity of mds.py:147-152
+// without the n x r^2 expansion), t = Q^T u (P u_i = q_i . t) and sum(u).
+// mean(z) follows in closed form from the constants Q^T 1 and Q^T Q, so a
+// Gram matvec costs one S' pass + one row pass and two grid barriers.
 //
-// One cooperative launch (one CTA per SM) runs the whole loop; every
-// reduction is block-deterministic (fixed shuffle trees) and the grid-level
-// combine runs in fixed block order, so results are bit-reproducible and the
-// stopping decisions are identical in every CTA.
+// Layout: one CTA per SM (cooperative launch); CTA c owns a contiguous row
+// slice and keeps that slice of the factor resident in shared memory for the
+// whole run (f64 rows, or int8 codes x per-column scales for large n; the
+// global-memory path is the fallback).  Every reduction has a fixed order
+// (register tiles -> fixed smem combine -> fixed block order), so results
+// are bit-reproducible and every stopping decision is identical in every CTA.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -27,31 +32,36 @@ namespace cg = cooperative_groups;
 
 namespace rfxc {
 
-constexpr int MDS_THREADS = 512;
-constexpr int MDS_WARPS = MDS_THREADS / 32;
-constexpr int MDS_CH = 32;          // rows staged per chunk in the S pass
-constexpr int MDS_MAXE = 8;         // S-pass entries per thread per sweep
-constexpr int MDS_SMEM_S_MAX = 96;  // r above this keeps S in global memory
-constexpr int SLOT = 8;             // small-reduction slots per CTA
+constexpr int MT = 512;             // threads per CTA
+constexpr int MW = MT / 32;         // warps per CTA
+constexpr int SLOTS = 24;           // small-reduction slots per CTA
+constexpr int SMEM_BUDGET = 220 * 1024;
+
+enum { QS_F64 = 0, QS_I8 = 1, QS_GLOBAL = 2 };
 
 struct MdsArgs {
-    const double* dq;
+    const double* dq;       // (n, r) f64 dequantised factor (global)
+    const int8_t* codes;    // (n, r) int8 codes (QS_I8) or null
+    const double* scales;   // (r) per-column scales (QS_I8)
     int64_t n;
     int r;
     double pmax;
     int k;
     int max_it;
     double tol;
-    int mode;  // 0: full MDS, 1: one gram_matvec of V[0] into w
-    double* V;       // k x n: start vectors in, found vectors out
-    double* w;       // n
-    double* z;       // n
-    double* parts;   // 2 x gridDim x SLOT (small reductions, double-buffered)
-    double* sparts;  // gridDim x P2 (S-pass partials)
-    double* tot;     // P2 totals
-    double* Sg;      // r x r (global S when r > MDS_SMEM_S_MAX)
-    double* coords;  // n x k
-    double* info;    // k x 4
+    int mode;               // 0: MDS, 1: one gram_matvec of V[0] into w
+    int qs;                 // QS_* storage of the factor slice
+    int s_in_smem;          // S' (r+1)^2 in shared memory
+    int64_t rpb;            // rows per CTA
+    double* V;              // k x n: start vectors in, found vectors out
+    double* w;              // n
+    double* parts;          // 2 x grid x SLOTS (small reductions, double-buffered)
+    double* sparts;         // grid x (E + 8) (S' partials + deflation dots)
+    double* tot;            // E + 8: totals of the current matvec
+    double* cst;            // E: constants Q'^T Q' (G = Q^T Q, c = Q^T 1, n)
+    double* Sg;             // grid x (r+1)^2 expanded S' (global fallback)
+    double* coords;         // n x k
+    double* info;           // k x 4
     int32_t* k_used;
 };
 
@@ -59,50 +69,66 @@ struct Ctx {
     cg::grid_group grid;
     int64_t r0, r1;
     int parity;
-    double* red;      // smem scratch 32
-    double* bcast;    // smem SLOT
+    double* red;     // >= 32
+    double* bcast;   // SLOTS
 };
 
+__host__ __device__ __forceinline__ int ntile(int r) { return (r + 1 + 3) / 4; }
+__host__ __device__ __forceinline__ int nentry(int r)
+{
+    const int t = ntile(r);
+    return 16 * t * (t + 1) / 2;
+}
+
+// ---------------------------------------------------------------- reductions
+// Sum m (<= SLOTS) per-thread values over the grid; every thread gets totals.
 __device__ void grid_sum(Ctx& C, const MdsArgs& A, double* v, int m)
 {
-    double* parts = A.parts + (int64_t)C.parity * gridDim.x * SLOT;
+    double* parts = A.parts + (int64_t)C.parity * gridDim.x * SLOTS;
     C.parity ^= 1;
     for (int j = 0; j < m; j++) {
-        double s = block_sum(v[j], C.red);
-        if (threadIdx.x == 0) parts[blockIdx.x * SLOT + j] = s;
-        __syncthreads();
+        const double s = block_sum(v[j], C.red);
+        if (threadIdx.x == 0) parts[blockIdx.x * SLOTS + j] = s;
     }
     C.grid.sync();
-    if (threadIdx.x < 32) {
-        for (int j = 0; j < m; j++) {
-            double s = 0.0;
-            for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += parts[b * SLOT + j];
-            s = warp_sum(s);
-            if (threadIdx.x == 0) C.bcast[j] = s;
-        }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = warp; j < m; j += MW) {  // one warp per slot, fixed order
+        double s = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) s += parts[b * SLOTS + j];
+        s = warp_sum(s);
+        if (lane == 0) C.bcast[j] = s;
     }
     __syncthreads();
     for (int j = 0; j < m; j++) v[j] = C.bcast[j];
     __syncthreads();
 }
 
-__device__ double grid_max(Ctx& C, const MdsArgs& A, double v)
+// max of `mx` and sum of `sm` in one barrier
+__device__ void grid_max_sum(Ctx& C, const MdsArgs& A, double& mx, double& sm)
 {
-    double* parts = A.parts + (int64_t)C.parity * gridDim.x * SLOT;
+    double* parts = A.parts + (int64_t)C.parity * gridDim.x * SLOTS;
     C.parity ^= 1;
-    double s = block_max(v, C.red);
-    if (threadIdx.x == 0) parts[blockIdx.x * SLOT] = s;
+    const double bm = block_max(mx, C.red);
+    const double bs = block_sum(sm, C.red);
+    if (threadIdx.x == 0) {
+        parts[blockIdx.x * SLOTS] = bm;
+        parts[blockIdx.x * SLOTS + 1] = bs;
+    }
     C.grid.sync();
-    if (threadIdx.x < 32) {
-        double m = -INFINITY;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) m = fmax(m, parts[b * SLOT]);
-        m = warp_max(m);
-        if (threadIdx.x == 0) C.bcast[0] = m;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp < 2) {
+        double s = warp == 0 ? -INFINITY : 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) {
+            const double x = parts[b * SLOTS + warp];
+            s = warp == 0 ? fmax(s, x) : s + x;
+        }
+        s = warp == 0 ? warp_max(s) : warp_sum(s);
+        if (lane == 0) C.bcast[warp] = s;
     }
     __syncthreads();
-    double out = C.bcast[0];
+    mx = C.bcast[0];
+    sm = C.bcast[1];
     __syncthreads();
-    return out;
 }
 
 // (max |x|, first index) over the grid
@@ -111,278 +137,366 @@ __device__ int64_t grid_argmax_abs(Ctx& C, const MdsArgs& A, const double* x)
     double bv = -1.0;
     int64_t bi = INT64_MAX;
     for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) {
-        double a = fabs(x[i]);
+        const double a = fabs(x[i]);
         if (a > bv) { bv = a; bi = i; }
     }
-    // warp then block
     for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    __shared__ double wv[MDS_WARPS];
-    __shared__ int64_t wi[MDS_WARPS];
+    __shared__ double wv[MW];
+    __shared__ int64_t wi[MW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
     __syncthreads();
-    double* parts = A.parts + (int64_t)C.parity * gridDim.x * SLOT;
+    double* parts = A.parts + (int64_t)C.parity * gridDim.x * SLOTS;
     C.parity ^= 1;
     if (threadIdx.x == 0) {
         double v = wv[0];
         int64_t ii = wi[0];
-        for (int w = 1; w < MDS_WARPS; w++)
+        for (int w = 1; w < MW; w++)
             if (wv[w] > v || (wv[w] == v && wi[w] < ii)) { v = wv[w]; ii = wi[w]; }
-        parts[blockIdx.x * SLOT] = v;
-        parts[blockIdx.x * SLOT + 1] = __longlong_as_double((long long)ii);
+        parts[blockIdx.x * SLOTS] = v;
+        parts[blockIdx.x * SLOTS + 1] = __longlong_as_double((long long)ii);
     }
     C.grid.sync();
     if (threadIdx.x == 0) {
         double v = -1.0;
         int64_t ii = INT64_MAX;
         for (int b = 0; b < (int)gridDim.x; b++) {
-            double pv = parts[b * SLOT];
-            int64_t pi = (int64_t)__double_as_longlong(parts[b * SLOT + 1]);
+            const double pv = parts[b * SLOTS];
+            const int64_t pi = (int64_t)__double_as_longlong(parts[b * SLOTS + 1]);
             if (pv > v || (pv == v && pi < ii)) { v = pv; ii = pi; }
         }
         C.bcast[0] = __longlong_as_double((long long)ii);
     }
     __syncthreads();
-    int64_t out = (int64_t)__double_as_longlong(C.bcast[0]);
+    const int64_t out = (int64_t)__double_as_longlong(C.bcast[0]);
     __syncthreads();
     return out;
 }
 
-__device__ __forceinline__ void tri_decode(int e, int r, int& a, int& b)
+// ------------------------------------------------------------- factor rows
+struct Rows {
+    int qs;
+    int r;
+    const double* f64;   // smem (QS_F64) or global (QS_GLOBAL), row stride r
+    const int8_t* i8;    // smem (QS_I8), row stride r
+    const double* sc;    // smem scales (QS_I8)
+    int64_t base;        // first global row of the slice (QS_GLOBAL indexing)
+
+    // q'_{row, col} of the augmented factor [Q | 1 | 0 ...]; row is slice-local
+    __device__ __forceinline__ double q(int64_t row, int col) const
+    {
+        if (col < r) {
+            if (qs == QS_I8) return (double)i8[row * r + col] * sc[col];
+            if (qs == QS_F64) return f64[row * r + col];
+            return __ldg(f64 + (base + row) * r + col);
+        }
+        return col == r ? 1.0 : 0.0;
+    }
+};
+
+__host__ __device__ __forceinline__ int tile_index(int ta, int tb, int T)
 {
-    // row-major upper triangle incl. diagonal: row a has r - a entries
-    double R = 2.0 * r + 1.0;
-    int aa = (int)((R - sqrt(R * R - 8.0 * e)) * 0.5);
-    aa = max(0, min(r - 1, aa));
-    while (aa > 0 && aa * r - aa * (aa - 1) / 2 > e) aa--;
-    while (aa + 1 < r && (aa + 1) * r - (aa + 1) * aa / 2 <= e) aa++;
-    a = aa;
-    b = a + (e - (a * r - a * (a - 1) / 2));
+    return ta * T - ta * (ta - 1) / 2 + (tb - ta);  // ta <= tb
+}
+
+// S' partial of this CTA: sum over slice rows of u_i q'_i q'_i^T as 4x4
+// register tiles of the upper triangle; row groups split the slice and are
+// combined in a fixed order.  Writes nentry(r) values to `out`.
+__device__ void spass(const Rows& Q, const double* us, int64_t rows, double* out,
+                      double* scratch)
+{
+    const int T = ntile(Q.r);
+    const int tiles = T * (T + 1) / 2;
+    const int tid = threadIdx.x;
+    if (tiles > MT) {  // large r: every thread owns whole tiles, all rows
+        for (int tile = tid; tile < tiles; tile += MT) {
+            int ta = 0, rem = tile;
+            while (rem >= T - ta) { rem -= T - ta; ta++; }
+            const int tb = ta + rem;
+            double acc[16];
+#pragma unroll
+            for (int e = 0; e < 16; e++) acc[e] = 0.0;
+            for (int64_t i = 0; i < rows; i++) {
+                const double u = us[i];
+                double qa[4], qb[4];
+#pragma unroll
+                for (int x = 0; x < 4; x++) {
+                    qa[x] = u * Q.q(i, 4 * ta + x);
+                    qb[x] = Q.q(i, 4 * tb + x);
+                }
+#pragma unroll
+                for (int x = 0; x < 4; x++)
+#pragma unroll
+                    for (int y = 0; y < 4; y++) acc[4 * x + y] += qa[x] * qb[y];
+            }
+#pragma unroll
+            for (int e = 0; e < 16; e++) out[tile * 16 + e] = acc[e];
+        }
+        __syncthreads();
+        return;
+    }
+    const int groups = MT / tiles;
+    const int g = tid / tiles, tile = tid % tiles;
+    double acc[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) acc[e] = 0.0;
+    int ta = 0, rem = tile;
+    while (rem >= T - ta) { rem -= T - ta; ta++; }
+    const int tb = ta + rem;
+    for (int tt = tid; tt < tiles * 16; tt += MT) scratch[tt] = 0.0;
+    if (g < groups) {
+        for (int64_t i = g; i < rows; i += groups) {
+            const double u = us[i];
+            double qa[4], qb[4];
+#pragma unroll
+            for (int x = 0; x < 4; x++) {
+                qa[x] = u * Q.q(i, 4 * ta + x);
+                qb[x] = Q.q(i, 4 * tb + x);
+            }
+#pragma unroll
+            for (int x = 0; x < 4; x++)
+#pragma unroll
+                for (int y = 0; y < 4; y++) acc[4 * x + y] += qa[x] * qb[y];
+        }
+    }
+    __syncthreads();
+    for (int gg = 0; gg < groups; gg++) {  // fixed combine order
+        if (g == gg) {
+#pragma unroll
+            for (int e = 0; e < 16; e++) scratch[tile * 16 + e] += acc[e];
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < tiles * 16; e += MT) out[e] = scratch[e];
+    __syncthreads();
+}
+
+// S'[a][b] from the tiled upper triangle (any a, b)
+__device__ __forceinline__ double sprime(const double* tot, int a, int b, int T)
+{
+    if (a > b) { const int s = a; a = b; b = s; }
+    const int ta = a >> 2, tb = b >> 2, x = a & 3, y = b & 3;
+    return tot[16 * tile_index(ta, tb, T) + 4 * x + y];
 }
 
 // y = G x - sum_{f<nf} lam_f (v_f . x) v_f   (deflated_matvec, mds.py:203-207)
-__device__ void matvec(Ctx& C, const MdsArgs& A, const double* x, double* y, int nf,
-                       const double* lam, double* Ssm, double* stage)
+// sx: sum of x over all rows.  Two grid barriers.
+__device__ void matvec(Ctx& C, const MdsArgs& A, const Rows& Q, const double* x, double sx,
+                       double* y, int nf, const double* lam, double* Ssm, double* us,
+                       double* scratch)
 {
-    const int r = A.r;
-    const int64_t n = A.n;
-    const int ntri = r * (r + 1) / 2;
-    const int P2 = ntri + r + 1 + nf;
-    // mean of x
-    double s1[1] = {0.0};
-    for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) s1[0] += x[i];
-    grid_sum(C, A, s1, 1);
-    const double mean = s1[0] / (double)n;
-
-    // S pass: entries [0,ntri) S upper, [ntri, ntri+r) t, ntri+r: su, then d_f
-    double* qs = stage;                  // MDS_CH x r
-    double* us = stage + MDS_CH * r;     // MDS_CH
-    double* xs = us + MDS_CH;            // MDS_CH
-    double* out = A.sparts + (int64_t)blockIdx.x * P2;
-    for (int ebase = 0; ebase < P2; ebase += MDS_THREADS * MDS_MAXE) {
-        double acc[MDS_MAXE];
-        int ea[MDS_MAXE], eb[MDS_MAXE];
-#pragma unroll
-        for (int q = 0; q < MDS_MAXE; q++) {
-            acc[q] = 0.0;
-            const int e = ebase + threadIdx.x + q * MDS_THREADS;
-            ea[q] = -1;
-            eb[q] = -1;
-            if (e < ntri) tri_decode(e, r, ea[q], eb[q]);
-            else if (e < ntri + r) { ea[q] = e - ntri; eb[q] = -2; }
-            else if (e == ntri + r) { ea[q] = -3; }
-            else if (e < P2) { ea[q] = -4; eb[q] = e - ntri - r - 1; }
-        }
-        for (int64_t base = C.r0; base < C.r1; base += MDS_CH) {
-            const int m = (int)min64(MDS_CH, C.r1 - base);
-            for (int t = threadIdx.x; t < m * r; t += blockDim.x)
-                qs[t] = A.dq[base * r + t];
-            for (int t = threadIdx.x; t < m; t += blockDim.x) {
-                xs[t] = x[base + t];
-                us[t] = x[base + t] - mean;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < MDS_MAXE; q++) {
-                const int a = ea[q], b = eb[q];
-                if (a == -1 && b == -1) continue;
-                double s = acc[q];
-                if (a >= 0 && b >= 0) {
-                    for (int t = 0; t < m; t++) s += us[t] * qs[t * r + a] * qs[t * r + b];
-                } else if (a >= 0) {
-                    for (int t = 0; t < m; t++) s += us[t] * qs[t * r + a];
-                } else if (a == -3) {
-                    for (int t = 0; t < m; t++) s += us[t];
-                } else {
-                    const double* vf = A.V + (int64_t)b * n + base;
-                    for (int t = 0; t < m; t++) s += vf[t] * xs[t];
-                }
-                acc[q] = s;
-            }
-            __syncthreads();
-        }
-#pragma unroll
-        for (int q = 0; q < MDS_MAXE; q++) {
-            const int e = ebase + threadIdx.x + q * MDS_THREADS;
-            if (e < P2) out[e] = acc[q];
+    const int r = A.r, T = ntile(r), E = nentry(r);
+    const int64_t n = A.n, rows = C.r1 - C.r0;
+    const double mean = sx / (double)n;
+    for (int64_t i = threadIdx.x; i < rows; i += MT) us[i] = x[C.r0 + i] - mean;
+    double dl[8];
+    for (int f = 0; f < nf; f++) dl[f] = 0.0;
+    for (int64_t i = threadIdx.x; i < rows; i += MT)
+        for (int f = 0; f < nf; f++) dl[f] += A.V[(int64_t)f * n + C.r0 + i] * x[C.r0 + i];
+    __syncthreads();
+    double* out = A.sparts + (int64_t)blockIdx.x * (E + 8);
+    spass(Q, us, rows, out, scratch);
+    for (int f = 0; f < nf; f++) {
+        const double s = block_sum(dl[f], C.red);
+        if (threadIdx.x == 0) out[E + f] = s;
+    }
+    C.grid.sync();
+    {  // distributed final reduce: one warp per entry, lanes over blocks
+        const int lane = threadIdx.x & 31;
+        const int gw = blockIdx.x * MW + (threadIdx.x >> 5), nw = gridDim.x * MW;
+        for (int e = gw; e < E + nf; e += nw) {
+            double s = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32)
+                s += A.sparts[(int64_t)b * (E + 8) + e];
+            s = warp_sum(s);
+            if (lane == 0) A.tot[e] = s;
         }
     }
     C.grid.sync();
-    // distributed final reduce of the S-pass partials (fixed block order)
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < P2; e += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < (int)gridDim.x; b++) s += A.sparts[(int64_t)b * P2 + e];
-        A.tot[e] = s;
-    }
-    C.grid.sync();
-    // expand S (symmetric) into smem or global
-    double* S = (r <= MDS_SMEM_S_MAX) ? Ssm : A.Sg;
-    if (r <= MDS_SMEM_S_MAX) {
-        for (int e = threadIdx.x; e < ntri; e += blockDim.x) {
-            int a, b;
-            tri_decode(e, r, a, b);
-            const double v = A.tot[e];
-            S[a * r + b] = v;
-            S[b * r + a] = v;
-        }
-        __syncthreads();
-    } else {
-        for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ntri; e += gridDim.x * blockDim.x) {
-            int a, b;
-            tri_decode(e, r, a, b);
-            const double v = A.tot[e];
-            S[a * r + b] = v;
-            S[b * r + a] = v;
-        }
-        C.grid.sync();
-    }
-    const double* t = A.tot + ntri;
-    const double su = A.tot[ntri + r];
+    const int ra = r + 1;
+    double* S = A.s_in_smem ? Ssm : A.Sg + (int64_t)blockIdx.x * ra * ra;
+    for (int e = threadIdx.x; e < ra * ra; e += MT) S[e] = sprime(A.tot, e / ra, e % ra, T);
+    __syncthreads();
+    const double su = S[r * ra + r];
     const double pm = A.pmax;
-    // z_i = pmax^2 su - 2 pmax (q_i.t) + q_i^T S q_i   (mds.py:179)
+    double ct, sgm;  // c.t and <S, G>
+    {
+        double a = 0.0, b = 0.0;
+        for (int e = threadIdx.x; e < r * r; e += MT)
+            b += S[(e / r) * ra + (e % r)] * sprime(A.cst, e / r, e % r, T);
+        for (int aa = threadIdx.x; aa < r; aa += MT) a += sprime(A.cst, aa, r, T) * S[aa * ra + r];
+        ct = block_sum(a, C.red);
+        sgm = block_sum(b, C.red);
+    }
+    const double mz = (pm * pm) * su - 2.0 * pm * ct / (double)n + sgm / (double)n;
+    const double* d = A.tot + E;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* qrow = stage + MDS_CH * r + 2 * MDS_CH + warp * r;
-    double zloc = 0.0;
-    for (int64_t i = C.r0 + warp; i < C.r1; i += MDS_WARPS) {
-        for (int a = lane; a < r; a += 32) qrow[a] = A.dq[i * r + a];
-        __syncwarp();
+    for (int64_t i = warp; i < rows; i += MW) {
         double pu = 0.0, ppu = 0.0;
         for (int a = lane; a < r; a += 32) {
             double sa = 0.0;
-            for (int b = 0; b < r; b++) sa += S[b * r + a] * qrow[b];
-            ppu += qrow[a] * sa;
-            pu += qrow[a] * t[a];
+            for (int b = 0; b < r; b++) sa += S[b * ra + a] * Q.q(i, b);
+            const double qa = Q.q(i, a);
+            ppu += qa * sa;
+            pu += qa * S[a * ra + r];
         }
         pu = warp_sum(pu);
         ppu = warp_sum(ppu);
-        const double zi = (pm * pm) * su - 2.0 * pm * pu + ppu;
-        if (lane == 0) A.z[i] = zi;
-        zloc += (lane == 0) ? zi : 0.0;
-        __syncwarp();
-    }
-    __syncthreads();
-    double s2[1] = {zloc};
-    grid_sum(C, A, s2, 1);
-    const double mz = s2[0] / (double)n;
-    // y = -1/2 (z - mean z) - sum_f lam_f d_f v_f
-    const double* d = A.tot + ntri + r + 1;
-    for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) {
-        double yi = -0.5 * (A.z[i] - mz);
-        for (int f = 0; f < nf; f++) yi -= lam[f] * d[f] * A.V[(int64_t)f * n + i];
-        y[i] = yi;
+        if (lane == 0) {
+            const double zi = (pm * pm) * su - 2.0 * pm * pu + ppu;
+            double yi = -0.5 * (zi - mz);
+            for (int f = 0; f < nf; f++) yi -= lam[f] * d[f] * A.V[(int64_t)f * n + C.r0 + i];
+            y[C.r0 + i] = yi;
+        }
     }
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(MDS_THREADS, 1) mds_kernel(MdsArgs A)
+__global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
 {
-    extern __shared__ double msm[];
+    extern __shared__ __align__(16) unsigned char msm[];
     __shared__ double red[32];
-    __shared__ double bcast[SLOT];
+    __shared__ double bcast[SLOTS];
     __shared__ double lam_s[8];
-    const int r = A.r;
-    double* Ssm = msm;                                       // r*r if small
-    double* stage = msm + (r <= MDS_SMEM_S_MAX ? r * r : 0); // staging
+    const int r = A.r, ra = r + 1, T = ntile(r), E = nentry(r);
     Ctx C{cg::this_grid(), 0, 0, 0, red, bcast};
     const int64_t n = A.n;
-    const int64_t rpb = (n + gridDim.x - 1) / gridDim.x;
-    C.r0 = min64(n, blockIdx.x * rpb);
-    C.r1 = min64(n, C.r0 + rpb);
+    C.r0 = min64(n, blockIdx.x * A.rpb);
+    C.r1 = min64(n, C.r0 + A.rpb);
+    const int64_t rows = C.r1 - C.r0;
+
+    // shared memory: [S'] [tile scratch] [u] [factor slice]
+    double* Ssm = reinterpret_cast<double*>(msm);
+    double* scratch = Ssm + (A.s_in_smem ? ra * ra : 0);
+    double* us = scratch + 16 * T * (T + 1) / 2;
+    unsigned char* qbase = reinterpret_cast<unsigned char*>(us + A.rpb);
+    Rows Q{A.qs, r, nullptr, nullptr, nullptr, C.r0};
+    if (A.qs == QS_F64) {
+        double* qs = reinterpret_cast<double*>(qbase);
+        for (int64_t e = threadIdx.x; e < rows * r; e += MT) qs[e] = A.dq[C.r0 * r + e];
+        Q.f64 = qs;
+    } else if (A.qs == QS_I8) {
+        double* sc = reinterpret_cast<double*>(qbase);
+        int8_t* qs = reinterpret_cast<int8_t*>(sc + r);
+        for (int e = threadIdx.x; e < r; e += MT) sc[e] = A.scales[e];
+        for (int64_t e = threadIdx.x; e < rows * r; e += MT) qs[e] = A.codes[C.r0 * r + e];
+        Q.i8 = qs;
+        Q.sc = sc;
+    } else {
+        Q.f64 = A.dq;
+    }
+    __syncthreads();
+
+    {  // constants Q'^T Q' (G = Q^T Q, c = Q^T 1) with u = 1
+        for (int64_t i = threadIdx.x; i < rows; i += MT) us[i] = 1.0;
+        __syncthreads();
+        double* out = A.sparts + (int64_t)blockIdx.x * (E + 8);
+        spass(Q, us, rows, out, scratch);
+        C.grid.sync();
+        const int lane = threadIdx.x & 31;
+        const int gw = blockIdx.x * MW + (threadIdx.x >> 5), nw = gridDim.x * MW;
+        for (int e = gw; e < E; e += nw) {
+            double s = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32)
+                s += A.sparts[(int64_t)b * (E + 8) + e];
+            s = warp_sum(s);
+            if (lane == 0) A.cst[e] = s;
+        }
+        C.grid.sync();
+    }
 
     if (A.mode == 1) {
-        matvec(C, A, A.V, A.w, 0, lam_s, Ssm, stage);
+        double s[1] = {0.0};
+        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) s[0] += A.V[i];
+        grid_sum(C, A, s, 1);
+        matvec(C, A, Q, A.V, s[0], A.w, 0, lam_s, Ssm, us, scratch);
         return;
     }
+
     int kused = 0;
     for (int comp = 0; comp < A.k; comp++) {
         double* v = A.V + (int64_t)comp * n;
-        for (int f = 0; f < comp; f++) {
+        for (int f = 0; f < comp; f++) {  // start vector: sequential Gram-Schmidt
             const double* vf = A.V + (int64_t)f * n;
-            double d[1] = {0.0};
-            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) d[0] += vf[i] * v[i];
-            grid_sum(C, A, d, 1);
-            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) v[i] -= d[0] * vf[i];
+            double dd[1] = {0.0};
+            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) dd[0] += vf[i] * v[i];
+            grid_sum(C, A, dd, 1);
+            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) v[i] -= dd[0] * vf[i];
             __syncthreads();
         }
         double nn[1] = {0.0};
-        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) nn[0] += v[i] * v[i];
+        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) nn[0] += v[i] * v[i];
         grid_sum(C, A, nn, 1);
         const double nv = sqrt(nn[0]);
         if (nv == 0.0) break;
-        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) v[i] /= nv;
-        __syncthreads();
+        double sv[1] = {0.0};
+        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) {
+            v[i] /= nv;
+            sv[0] += v[i];
+        }
+        grid_sum(C, A, sv, 1);
+        double sumv = sv[0];
 
         double lam = 0.0;
         bool conv = false;
         int it = 0;
         for (it = 1; it <= A.max_it; it++) {
-            matvec(C, A, v, A.w, comp, lam_s, Ssm, stage);
+            matvec(C, A, Q, v, sumv, A.w, comp, lam_s, Ssm, us, scratch);
+            // all projections in one reduction: e_f = v_f.w, g_f = v_f.v, v.w, w.w
+            double dots[2 * 8 + 2];
+            const int m = 2 * comp + 2;
+            for (int j = 0; j < m; j++) dots[j] = 0.0;
+            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) {
+                const double wi = A.w[i], vi = v[i];
+                for (int f = 0; f < comp; f++) {
+                    const double vf = A.V[(int64_t)f * n + i];
+                    dots[2 * f] += vf * wi;
+                    dots[2 * f + 1] += vf * vi;
+                }
+                dots[2 * comp] += vi * wi;
+                dots[2 * comp + 1] += wi * wi;
+            }
+            grid_sum(C, A, dots, m);
+            // w' = w - sum_f e_f v_f (orthonormal v_f): v.w' and |w'|^2 in closed form
+            lam = dots[2 * comp];
+            double nw2 = dots[2 * comp + 1];
             for (int f = 0; f < comp; f++) {
-                const double* vf = A.V + (int64_t)f * n;
-                double d[1] = {0.0};
-                for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x)
-                    d[0] += vf[i] * A.w[i];
-                grid_sum(C, A, d, 1);
-                for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x)
-                    A.w[i] -= d[0] * vf[i];
-                __syncthreads();
+                lam -= dots[2 * f] * dots[2 * f + 1];
+                nw2 -= dots[2 * f] * dots[2 * f];
             }
-            double lw[2] = {0.0, 0.0};
-            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) {
-                lw[0] += v[i] * A.w[i];
-                lw[1] += A.w[i] * A.w[i];
-            }
-            grid_sum(C, A, lw, 2);
-            lam = lw[0];
-            const double nw = sqrt(lw[1]);
+            const double nw = sqrt(fmax(nw2, 0.0));
             if (nw == 0.0) {
                 lam = 0.0;
                 conv = true;
                 break;
             }
             const double sg = (lam / nw < 0.0) ? -1.0 : 1.0;  // sign of v_new . v
-            double dmax = 0.0;
-            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) {
-                double vn = A.w[i] / nw;
+            double dmax = 0.0, snew = 0.0;
+            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) {
+                double wi = A.w[i];
+                for (int f = 0; f < comp; f++) wi -= dots[2 * f] * A.V[(int64_t)f * n + i];
+                double vn = wi / nw;
                 if (sg < 0) vn = -vn;
                 dmax = fmax(dmax, fabs(vn - v[i]));
                 v[i] = vn;
+                snew += vn;
             }
-            const double delta = grid_max(C, A, dmax);
-            if (delta < A.tol) {
+            grid_max_sum(C, A, dmax, snew);
+            sumv = snew;
+            if (dmax < A.tol) {
                 conv = true;
                 break;
             }
         }
         if (it > A.max_it) it = A.max_it;
         // residual |deflated_matvec(v) - lam v| / |lam|  (mds.py:241-242)
-        matvec(C, A, v, A.w, comp, lam_s, Ssm, stage);
+        matvec(C, A, Q, v, sumv, A.w, comp, lam_s, Ssm, us, scratch);
         double rr[1] = {0.0};
-        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) {
+        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) {
             const double e = A.w[i] - lam * v[i];
             rr[0] += e * e;
         }
@@ -399,73 +513,98 @@ __global__ void __launch_bounds__(MDS_THREADS, 1) mds_kernel(MdsArgs A)
         }
         kused = comp + 1;
     }
-    // coordinates: sqrt(lambda) * sign-fixed v  (mds.py:83-86, :257-261)
     for (int c = 0; c < kused; c++) {
         const double* v = A.V + (int64_t)c * n;
         const int64_t idx = grid_argmax_abs(C, A, v);
-        const double sg = v[idx] < 0.0 ? -1.0 : 1.0;
+        const double sgn = v[idx] < 0.0 ? -1.0 : 1.0;
         const double sl = sqrt(lam_s[c]);
-        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x)
-            A.coords[i * A.k + c] = sl * (sg < 0 ? -v[i] : v[i]);
+        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT)
+            A.coords[i * A.k + c] = sl * (sgn < 0 ? -v[i] : v[i]);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *A.k_used = kused;
 }
 
+// ------------------------------------------------------------------- host
 struct Layout {
-    int64_t V, w, z, parts, sparts, tot, Sg, bytes;
+    int64_t V, w, parts, sparts, tot, cst, Sg, bytes;
 };
 
-static int mds_grid()
-{
-    static int g = 0;
-    if (!g) {
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mds_kernel, MDS_THREADS,
-                                                      64 * 1024);
-        g = sm_count() * std::max(1, std::min(occ, 1));
-    }
-    return g;
-}
+static int grid_size() { return sm_count(); }
 
 static Layout mds_layout(int64_t n, int r, int k)
 {
-    const int G = mds_grid();
-    const int64_t P2 = (int64_t)r * (r + 1) / 2 + r + 1 + k;
+    const int G = grid_size();
+    const int64_t E = nentry(r);
     Layout L;
     int64_t o = 0;
-    auto take = [&](int64_t count) { int64_t at = o; o += ((count * 8 + 255) / 256) * 256; return at; };
+    auto take = [&](int64_t count) {
+        const int64_t at = o;
+        o += ((count * 8 + 255) / 256) * 256;
+        return at;
+    };
     L.V = take((int64_t)k * n);
     L.w = take(n);
-    L.z = take(n);
-    L.parts = take(2LL * G * SLOT);
-    L.sparts = take((int64_t)G * P2);
-    L.tot = take(P2);
-    L.Sg = take((int64_t)r * r);
+    L.parts = take(2LL * G * SLOTS);
+    L.sparts = take((int64_t)G * (E + 8));
+    L.tot = take(E + 8);
+    L.cst = take(E + 8);
+    L.Sg = take((int64_t)G * (r + 1) * (r + 1));
     L.bytes = o;
     return L;
 }
 
-static size_t mds_smem(int r)
+// choose the factor storage; returns the dynamic shared memory size
+static size_t plan_smem(MdsArgs& A)
 {
-    size_t s = (r <= MDS_SMEM_S_MAX ? (size_t)r * r : 0);
-    s += (size_t)MDS_CH * r + MDS_CH * 2 + (size_t)MDS_WARPS * r;
-    return s * 8;
+    const int r = A.r, ra = r + 1;
+    const int64_t T = ntile(r);
+    A.rpb = (A.n + grid_size() - 1) / grid_size();
+    const size_t s_bytes = (size_t)ra * ra * 8;
+    const size_t fixed = (size_t)(16 * T * (T + 1) / 2) * 8 + (size_t)A.rpb * 8;
+    const size_t f64_rows = (size_t)A.rpb * r * 8, i8_rows = (size_t)r * 8 + (size_t)A.rpb * r;
+    A.s_in_smem = s_bytes + fixed + i8_rows <= SMEM_BUDGET;
+    const size_t sb = A.s_in_smem ? s_bytes : 0;
+    if (sb + fixed + f64_rows <= SMEM_BUDGET) {
+        A.qs = QS_F64;
+        return sb + fixed + f64_rows;
+    }
+    if (A.codes && sb + fixed + i8_rows <= SMEM_BUDGET) {
+        A.qs = QS_I8;
+        return sb + fixed + i8_rows;
+    }
+    A.qs = QS_GLOBAL;
+    if (sb + fixed > SMEM_BUDGET) A.s_in_smem = 0;
+    return (A.s_in_smem ? s_bytes : 0) + fixed;
 }
 
 static int launch_mds(MdsArgs& A, cudaStream_t st)
 {
-    const size_t smem = mds_smem(A.r);
+    const size_t smem = plan_smem(A);
+    if (smem > SMEM_BUDGET)
+        return fail(RFXC_EDATA, "mds: n=%lld r=%d too large for one GPU", (long long)A.n, A.r);
     cudaError_t e = cudaFuncSetAttribute(mds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 1));
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "mds attr: %s", cudaGetErrorString(e));
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mds_kernel, MDS_THREADS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mds_kernel, MT, smem);
     if (occ < 1) return fail(RFXC_ERUNTIME, "mds: kernel does not fit an SM (r=%d)", A.r);
     void* args[] = {&A};
-    e = cudaLaunchCooperativeKernel((const void*)mds_kernel, dim3(mds_grid()), dim3(MDS_THREADS),
-                                    args, smem, st);
+    e = cudaLaunchCooperativeKernel((const void*)mds_kernel, dim3(grid_size()), dim3(MT), args,
+                                    smem, st);
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "mds launch: %s", cudaGetErrorString(e));
     return check_launch("mds");
+}
+
+static void bind(MdsArgs& A, const Layout& L, void* d_work)
+{
+    char* base = static_cast<char*>(d_work);
+    A.V = reinterpret_cast<double*>(base + L.V);
+    A.w = reinterpret_cast<double*>(base + L.w);
+    A.parts = reinterpret_cast<double*>(base + L.parts);
+    A.sparts = reinterpret_cast<double*>(base + L.sparts);
+    A.tot = reinterpret_cast<double*>(base + L.tot);
+    A.cst = reinterpret_cast<double*>(base + L.cst);
+    A.Sg = reinterpret_cast<double*>(base + L.Sg);
 }
 
 }  // namespace rfxc
@@ -477,17 +616,18 @@ extern "C" int64_t rfxc_mds_work_bytes(int64_t n, int32_t r, int32_t k)
     return mds_layout(n, r, std::max(k, 1)).bytes;
 }
 
-extern "C" int rfxc_mds_power(const double* d_dq, int64_t n, int32_t r, double pmax, int32_t k,
+extern "C" int rfxc_mds_power(const double* d_dq, const int8_t* d_codes, const double* d_scales,
+                              int64_t n, int32_t r, double pmax, int32_t k,
                               int32_t max_iterations, double tol, int64_t seed, double* d_coords,
                               double* d_info, int32_t* d_k_used, void* d_work, void* stream)
 {
     if (n < 1 || r < 1 || k < 1 || k > 8 || max_iterations < 1)
         return fail(RFXC_EDATA, "mds_power: bad arguments");
     cudaStream_t st = as_stream(stream);
-    Layout L = mds_layout(n, r, k);
-    char* base = static_cast<char*>(d_work);
-    MdsArgs A;
+    MdsArgs A{};
     A.dq = d_dq;
+    A.codes = d_codes;
+    A.scales = d_scales;
     A.n = n;
     A.r = r;
     A.pmax = pmax;
@@ -495,19 +635,13 @@ extern "C" int rfxc_mds_power(const double* d_dq, int64_t n, int32_t r, double p
     A.max_it = max_iterations;
     A.tol = tol;
     A.mode = 0;
-    A.V = reinterpret_cast<double*>(base + L.V);
-    A.w = reinterpret_cast<double*>(base + L.w);
-    A.z = reinterpret_cast<double*>(base + L.z);
-    A.parts = reinterpret_cast<double*>(base + L.parts);
-    A.sparts = reinterpret_cast<double*>(base + L.sparts);
-    A.tot = reinterpret_cast<double*>(base + L.tot);
-    A.Sg = reinterpret_cast<double*>(base + L.Sg);
+    bind(A, mds_layout(n, r, k), d_work);
     A.coords = d_coords;
     A.info = d_info;
     A.k_used = d_k_used;
     // start vectors Pcg32(seed + c, SEQ_POWER).normals(n)  (mds.py:210-211)
     for (int c = 0; c < k; c++) {
-        int rc = rfxc_normals(seed + c, 5, n, A.V + (int64_t)c * n, stream);
+        const int rc = rfxc_normals(seed + c, 5, n, A.V + (int64_t)c * n, stream);
         if (rc) return rc;
     }
     cudaMemsetAsync(d_info, 0, (size_t)k * 4 * 8, st);
@@ -520,8 +654,6 @@ extern "C" int rfxc_gram_matvec(const double* d_dq, int64_t n, int32_t r, double
 {
     if (n < 1 || r < 1) return fail(RFXC_EDATA, "gram_matvec: bad arguments");
     cudaStream_t st = as_stream(stream);
-    Layout L = mds_layout(n, r, 1);
-    char* base = static_cast<char*>(d_work);
     MdsArgs A{};
     A.dq = d_dq;
     A.n = n;
@@ -531,14 +663,9 @@ extern "C" int rfxc_gram_matvec(const double* d_dq, int64_t n, int32_t r, double
     A.max_it = 1;
     A.tol = 1.0;
     A.mode = 1;
-    A.V = reinterpret_cast<double*>(base + L.V);
+    bind(A, mds_layout(n, r, 1), d_work);
     A.w = d_w;
-    A.z = reinterpret_cast<double*>(base + L.z);
-    A.parts = reinterpret_cast<double*>(base + L.parts);
-    A.sparts = reinterpret_cast<double*>(base + L.sparts);
-    A.tot = reinterpret_cast<double*>(base + L.tot);
-    A.Sg = reinterpret_cast<double*>(base + L.Sg);
-    cudaError_t e = cudaMemcpyAsync(A.V, d_v, (size_t)n * 8, cudaMemcpyDeviceToDevice, st);
+    const cudaError_t e = cudaMemcpyAsync(A.V, d_v, (size_t)n * 8, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "gram_matvec copy: %s", cudaGetErrorString(e));
     return launch_mds(A, st);
 }

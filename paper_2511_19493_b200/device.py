@@ -10,12 +10,12 @@ HBM layout (one process per GPU):
   seg      (sum L + 1) int64 — start of every leaf's run in perm
   leaf_base (Bl + 1) int64 — global leaf id of each tree's leaf 0
 Everything stays on the device between calls; host arrays are produced
-only when a caller reads them.
+only when a caller reads them.  Uploads are packed on the host (multi-
+threaded C++, librfxc's host_pack.cpp) straight into pinned buffers so only
+the packed bytes cross PCIe.
 """
 
 from __future__ import annotations
-
-import warnings
 
 import numpy as np
 
@@ -29,129 +29,136 @@ def _torch():
     return torch
 
 
-def relayout_siblings(status, split_var, threshold, cat_mask, left, right):
-    """Renumber one tree breadth-first so that right == left + 1 for every
-    internal node (the packed layout stores only the left child).  Trees
-    grown by the trainer already satisfy this (_kernels.py:313-317); only
-    hand-built trees take this path.  Terminal order (and therefore the
-    dense leaf codes of forest.py:95-99) is preserved by carrying the
-    original node id and remapping codes after packing."""
-    nc = len(status)
-    order = [0]
-    newid = {0: 0}
-    q = 0
-    while q < len(order):
-        old = order[q]
-        q += 1
-        if status[old] == 0:
-            for ch in (left[old], right[old]):
-                newid[int(ch)] = len(order)
-                order.append(int(ch))
-    order = np.asarray(order, dtype=np.int64)
-    if len(order) != nc:
-        raise DataError("tree has unreachable nodes")
-    inv = np.empty(nc, dtype=np.int64)
-    inv[order] = np.arange(nc)
-    st = status[order]
-    lf = np.where(st == 0, inv[np.maximum(left[order], 0)], -1).astype(np.int32)
-    return (st, split_var[order], threshold[order], cat_mask[order], lf, order)
+def _pinned(nbytes: int):
+    """Pinned host staging buffer (torch caching host allocator) + numpy view."""
+    torch = _torch()
+    buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, pin_memory=True)
+    return buf, buf.numpy()
+
+
+def feature_bits(p: int) -> int:
+    fb = 1
+    while (1 << fb) < p:
+        fb += 1
+    return fb
+
+
+def _as(a, dtype):
+    a = np.asarray(a)
+    if a.dtype != dtype or not a.flags.c_contiguous:
+        a = np.ascontiguousarray(a, dtype=dtype)
+    return a
+
+
+class DeviceValues:
+    """Dataset.values on the GPU: f32 when every value is f32-exact (then the
+    f32 node layout compares exactly), else f64."""
+
+    def __init__(self, values: np.ndarray):
+        torch = _torch()
+        self.dev = _lib.require_cuda()
+        vals = np.asfortranarray(values, dtype=np.float64)
+        self.n, self.p = vals.shape
+        self._host = vals
+        buf, view = _pinned(vals.size * 4)
+        exact = np.zeros(1, dtype=np.int32)
+        # F-order (n, p) is exactly (p, n) row-major
+        _lib.call("rfxc_values_to_f32_host", vals.ctypes.data_as(_lib.P), vals.size,
+                  view.ctypes.data_as(_lib.P), exact.ctypes.data_as(_lib.P), 0)
+        self.exact_f32 = bool(exact[0])
+        self.f32 = buf.to(self.dev, non_blocking=True).view(torch.float32).view(self.p, self.n) \
+            if self.exact_f32 else None
+        self._f64 = None
+
+    @property
+    def f64(self):
+        torch = _torch()
+        if self._f64 is None:
+            self._f64 = torch.from_numpy(np.ascontiguousarray(self._host.T)).to(self.dev)
+        return self._f64
 
 
 class DeviceForest:
-    """Packed node records of trees [tree_lo, tree_hi) on the current GPU."""
+    """Packed node records of trees [tree_lo, tree_hi) of ``forest`` on the
+    current GPU (packed on the host, uploaded once)."""
 
-    def __init__(self, forest, tree_lo: int = 0, tree_hi: int | None = None):
+    def __init__(self, forest, tree_lo: int = 0, tree_hi: int | None = None,
+                 layout: int | None = None, nthreads: int = 0):
         torch = _torch()
         dev = _lib.require_cuda()
-        trees = forest.trees
-        tree_hi = len(trees) if tree_hi is None else tree_hi
-        self.tree_lo, self.tree_hi = tree_lo, tree_hi
+        trees = forest.trees[tree_lo:(len(forest.trees) if tree_hi is None else tree_hi)]
+        self.tree_lo = tree_lo
+        self.tree_hi = tree_lo + len(trees)
         self.p = int(forest.p)
-        col_cat = np.ascontiguousarray(getattr(forest, "col_cat", trees[0].col_cat),
-                                       dtype=np.uint8)
-        st, sv, th, cm, lf, counts, code_maps = [], [], [], [], [], [], []
-        for t in trees[tree_lo:tree_hi]:
-            s = np.asarray(t.status, np.int8)
-            l_ = np.asarray(t.left, np.int32)
-            r_ = np.asarray(t.right, np.int32)
-            internal = s == 0
-            if np.all(r_[internal] == l_[internal] + 1):
-                st.append(s); sv.append(np.asarray(t.split_var, np.int32))
-                th.append(np.asarray(t.threshold, np.float64))
-                cm.append(np.asarray(t.cat_mask, np.int64)); lf.append(l_)
-                code_maps.append(None)
-            else:
-                s2, sv2, th2, cm2, lf2, order = relayout_siblings(
-                    s, np.asarray(t.split_var, np.int32), np.asarray(t.threshold, np.float64),
-                    np.asarray(t.cat_mask, np.int64), l_, r_)
-                st.append(s2); sv.append(sv2); th.append(th2); cm.append(cm2); lf.append(lf2)
-                # packed code (leaf ordinal in new order) -> reference code
-                ref_code = np.cumsum(s == 1) - 1
-                code_maps.append(ref_code[order[s2 == 1]].astype(np.int32))
-            counts.append(len(s))
-        self.relaid = any(m is not None for m in code_maps)
-        leaf_code = None
-        if self.relaid:  # explicit per-node codes in the reference's terminal order
-            parts = []
-            for s_, m in zip(st, code_maps):
-                c = np.full(len(s_), -1, dtype=np.int32)
-                c[s_ == 1] = m if m is not None else np.arange(int((s_ == 1).sum()))
-                parts.append(c)
-            leaf_code = np.concatenate(parts)
-        self.node_counts = np.asarray(counts, dtype=np.int64)
-        self.leaf_counts = np.asarray([int((a == 1).sum()) for a in st], dtype=np.int32)
-        off = np.zeros(len(counts) + 1, dtype=np.int64)
-        off[1:] = np.cumsum(self.node_counts)
-        self.total_nodes = int(off[-1])
-        up = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-        self._raw = dict(status=up(np.concatenate(st)), split_var=up(np.concatenate(sv)),
-                         threshold=up(np.concatenate(th)), cat_mask=up(np.concatenate(cm)),
-                         left=up(np.concatenate(lf)))
-        self.leaf_code = up(leaf_code) if leaf_code is not None else None
-        self.node_off = up(off)
-        self.col_cat = up(col_cat)
-        self._packed = {}
-        fb = max(1, int(np.ceil(np.log2(max(self.p, 2)))))
-        self.f32_ok = int(self.node_counts.max()) < (1 << (31 - fb))
+        B = len(trees)
+        col_cat = _as(getattr(forest, "col_cat", trees[0].col_cat), np.uint8)
+        keep = []  # keep converted arrays alive during the call
+        tables = {name: np.empty(B, dtype=np.uintp) for name in
+                  ("status", "split_var", "threshold", "cat_mask", "left", "right")}
+        dts = {"status": np.int8, "split_var": np.int32, "threshold": np.float64,
+               "cat_mask": np.int64, "left": np.int32, "right": np.int32}
+        counts = np.empty(B, dtype=np.int64)
+        for b, t in enumerate(trees):
+            for name, dt in dts.items():
+                a = _as(getattr(t, name), dt)
+                keep.append(a)
+                tables[name][b] = a.ctypes.data
+            counts[b] = len(t.status)
+        self.node_counts = counts
+        self.total_nodes = int(counts.sum())
+        self.f32_ok = int(counts.max()) < (1 << (31 - feature_bits(self.p)))
+        if layout is None:
+            layout = _lib.NODES_F32 if self.f32_ok else _lib.NODES_F64
+        if layout == _lib.NODES_F32 and not self.f32_ok:
+            raise DataError("tree too large for the 8-byte node layout")
+        self.layout = layout
+        rec = 8 if layout == _lib.NODES_F32 else 16
+        buf, view = _pinned(self.total_nodes * rec)
+        off = np.empty(B + 1, dtype=np.int64)
+        lc = np.empty(B, dtype=np.int32)
+        P = _lib.P
+        with region("forest_pack_host"):
+            _lib.call("rfxc_forest_pack_host", *(tables[k].ctypes.data_as(P) for k in
+                                                 ("status", "split_var", "threshold",
+                                                  "cat_mask", "left", "right")),
+                      counts.ctypes.data_as(P), B, col_cat.ctypes.data_as(P), self.p, layout,
+                      view.ctypes.data_as(P), off.ctypes.data_as(P), lc.ctypes.data_as(P),
+                      nthreads)
+        del keep
+        self.leaf_counts = lc
+        self.nodes = buf.to(dev, non_blocking=True)
+        self.node_off = torch.from_numpy(off).to(dev)
 
     @property
     def ntree(self) -> int:
         return self.tree_hi - self.tree_lo
 
-    def packed(self, layout: int):
-        torch = _torch()
-        if layout not in self._packed:
-            nbytes = 8 if layout == _lib.NODES_F32 else 16
-            nodes = torch.empty(self.total_nodes * nbytes, dtype=torch.uint8,
-                                device=self.node_off.device)
-            lc = torch.empty(self.ntree, dtype=torch.int32, device=self.node_off.device)
-            r = self._raw
-            _lib.call("rfxc_forest_pack", _lib.ptr(r["status"]), _lib.ptr(r["split_var"]),
-                      _lib.ptr(r["threshold"]), _lib.ptr(r["cat_mask"]), _lib.ptr(r["left"]),
-                      _lib.ptr(self.leaf_code), _lib.ptr(self.node_off), self.ntree, self.total_nodes,
-                      _lib.ptr(self.col_cat), self.p, layout, _lib.ptr(nodes), _lib.ptr(lc),
-                      _lib.stream_handle())
-            self._packed[layout] = nodes
-        return self._packed[layout]
-
-
-class DeviceValues:
-    """Dataset.values on the GPU: f32 when every value is f32-exact."""
-
-    def __init__(self, values: np.ndarray):
+    @classmethod
+    def packed_on_device(cls, forest, layout: int):
+        """Reference-layout raw arrays uploaded as-is and packed by the device
+        kernel (rfxc_forest_pack); requires right == left + 1.  Returns the
+        packed node tensor, node offsets and leaf counts (device)."""
         torch = _torch()
         dev = _lib.require_cuda()
-        vals = np.asfortranarray(values, dtype=np.float64)
-        self.n, self.p = vals.shape
-        # F-order (n, p) is exactly (p, n) row-major
-        with warnings.catch_warnings():  # read-only Dataset.values: torch only reads it
-            warnings.simplefilter("ignore", UserWarning)
-            self.f64 = torch.from_numpy(vals.T).to(dev)
-        self.f32 = torch.empty((self.p, self.n), dtype=torch.float32, device=dev)
-        flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        _lib.call("rfxc_values_to_f32", _lib.ptr(self.f64), self.n * self.p,
-                  _lib.ptr(self.f32), _lib.ptr(flag), _lib.stream_handle())
-        self.exact_f32 = int(flag.item()) == 0
+        trees = forest.trees
+        cat = lambda name, dt: torch.from_numpy(
+            np.concatenate([_as(getattr(t, name), dt) for t in trees])).to(dev)
+        off = np.zeros(len(trees) + 1, dtype=np.int64)
+        off[1:] = np.cumsum([len(t.status) for t in trees])
+        total = int(off[-1])
+        nodes = torch.empty(total * (8 if layout == _lib.NODES_F32 else 16), dtype=torch.uint8,
+                            device=dev)
+        lc = torch.empty(len(trees), dtype=torch.int32, device=dev)
+        d_off = torch.from_numpy(off).to(dev)
+        col_cat = torch.from_numpy(_as(forest.col_cat, np.uint8)).to(dev)
+        st, sv, th = cat("status", np.int8), cat("split_var", np.int32), cat("threshold",
+                                                                                np.float64)
+        cm, lf = cat("cat_mask", np.int64), cat("left", np.int32)
+        _lib.call("rfxc_forest_pack", _lib.ptr(st), _lib.ptr(sv), _lib.ptr(th), _lib.ptr(cm),
+                  _lib.ptr(lf), _lib.ptr(None), _lib.ptr(d_off), len(trees), total,
+                  _lib.ptr(col_cat), int(forest.p), layout, _lib.ptr(nodes), _lib.ptr(lc),
+                  _lib.stream_handle())
+        return nodes, d_off, lc
 
 
 class DeviceMembership:
@@ -215,19 +222,20 @@ class DeviceMembership:
         return cls(nb, tm, lc, 0, B, B)
 
 
-def traverse(dforest: DeviceForest, dvalues: DeviceValues) -> DeviceMembership:
+def traverse(dforest: DeviceForest, dvalues: DeviceValues):
     """K1: codes of every sample in every local tree (tm and nb layouts)."""
     torch = _torch()
-    use_f32 = dvalues.exact_f32 and dforest.f32_ok
-    layout = _lib.NODES_F32 if use_f32 else _lib.NODES_F64
-    vals = dvalues.f32 if use_f32 else dvalues.f64
+    layout = dforest.layout
+    if layout == _lib.NODES_F32 and not dvalues.exact_f32:
+        raise DataError("f32 node layout needs f32-exact values")
+    vals = dvalues.f32 if layout == _lib.NODES_F32 else dvalues.f64
     n, Bl = dvalues.n, dforest.ntree
     dev = vals.device
     tm = torch.empty((Bl, n), dtype=torch.int32, device=dev)
-    nodes = dforest.packed(layout)
     with region("leaf_codes"):
-        _lib.call("rfxc_leaf_codes", _lib.ptr(nodes), _lib.ptr(dforest.node_off), layout,
-                  dvalues.p, 0, Bl, _lib.ptr(vals), n, _lib.ptr(tm), _lib.stream_handle())
+        _lib.call("rfxc_leaf_codes", _lib.ptr(dforest.nodes), _lib.ptr(dforest.node_off),
+                  layout, dvalues.p, 0, Bl, _lib.ptr(vals), n, _lib.ptr(tm),
+                  _lib.stream_handle())
     nb = torch.empty((n, Bl), dtype=torch.int32, device=dev)
     _lib.call("rfxc_transpose_i32", _lib.ptr(tm), Bl, n, _lib.ptr(nb), _lib.stream_handle())
     return nb, tm, layout

@@ -122,14 +122,21 @@ def mds_lowrank_device(lowrank: LowRankQuantized, config: PowerIterConfig | None
     dq = lowrank.dq if hasattr(lowrank, "dq") else lowrank.dequantized_device()
     n, r = dq.shape
     dev = dq.device
+    codes = scales = None
+    if lowrank.mode == "i8":  # int8 factor: shared-memory-resident slices at large n
+        if hasattr(lowrank, "data"):
+            codes, scales = lowrank.data, lowrank.scales
+        else:
+            codes, scales = lowrank.device_codes()
     coords = torch.empty((n, cfg.k), dtype=torch.float64, device=dev)
     info = torch.empty((cfg.k, 4), dtype=torch.float64, device=dev)
     kused = torch.empty(1, dtype=torch.int32, device=dev)
     work = _work(n, r, cfg.k, dev)
     with region("mds_power"):
-        _lib.call("rfxc_mds_power", _lib.ptr(dq), n, r, float(lowrank.pmax), cfg.k,
-                  cfg.max_iterations, float(cfg.tol), cfg.seed, _lib.ptr(coords),
-                  _lib.ptr(info), _lib.ptr(kused), _lib.ptr(work), _lib.stream_handle())
+        _lib.call("rfxc_mds_power", _lib.ptr(dq), _lib.ptr(codes), _lib.ptr(scales), n, r,
+                  float(lowrank.pmax), cfg.k, cfg.max_iterations, float(cfg.tol), cfg.seed,
+                  _lib.ptr(coords), _lib.ptr(info), _lib.ptr(kused), _lib.ptr(work),
+                  _lib.stream_handle())
     return coords, info, kused
 
 

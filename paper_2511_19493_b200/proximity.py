@@ -156,8 +156,9 @@ def leaf_membership(forest, dataset, trees: tuple | None = None) -> LeafMembersh
         if not 0 <= lo < hi <= B:
             raise DataError(f"tree range {trees} outside [0, {B})")
         local = (lo, hi)
-    dforest = DeviceForest(forest, *local)
     dvals = DeviceValues(dataset.values)
+    layout = None if dvals.exact_f32 else _lib.NODES_F64
+    dforest = DeviceForest(forest, *local, layout=layout)
     nb, tm, _ = traverse(dforest, dvals)
     dev = DeviceMembership(nb, tm, dforest.leaf_counts, lo, hi, B)
     return LeafMembership(leaf_counts=dforest.leaf_counts, _dev=dev)
@@ -442,14 +443,21 @@ class LowRankQuantized:
             self._dq = self.factor.dequantize()
         return self._dq
 
-    def dequantized_device(self):
-        """(n, r) f64 dequantised factor on the GPU."""
+    def device_codes(self):
+        """(data, scales) of the quantised factor on the GPU."""
         import torch
-        if self._dq_dev is None:
+        if getattr(self, "_codes_dev", None) is None:
             dev = _lib.require_cuda()
             data = torch.from_numpy(np.ascontiguousarray(self.factor.data)).to(dev)
             sc = None if self.factor.scales is None else torch.from_numpy(
                 np.ascontiguousarray(self.factor.scales)).to(dev)
+            self._codes_dev = (data, sc)
+        return self._codes_dev
+
+    def dequantized_device(self):
+        """(n, r) f64 dequantised factor on the GPU."""
+        if self._dq_dev is None:
+            data, sc = self.device_codes()
             n, r = self.n, int(np.prod(self.factor.shape)) // max(self.n, 1)
             self._dq_dev = device_dequantize(data, sc, n, r, self.mode)
         return self._dq_dev
@@ -620,9 +628,11 @@ class DeviceLowRank:
 
     def to_host(self) -> LowRankQuantized:
         qf = to_host(self.mode, (self.n, self.rank), self.data, self.scales)
-        return LowRankQuantized(n=self.n, rank=self.rank, mode=self.mode, factor=qf,
-                                pmax=self.pmax, tree_count=self.tree_count,
-                                rank_degraded=self.degraded, _dq_dev=self.dq)
+        out = LowRankQuantized(n=self.n, rank=self.rank, mode=self.mode, factor=qf,
+                               pmax=self.pmax, tree_count=self.tree_count,
+                               rank_degraded=self.degraded, _dq_dev=self.dq)
+        out._codes_dev = (self.data, self.scales)
+        return out
 
 
 def lowrank_proximity(membership: LeafMembership, rank: int, mode: str = "i8",

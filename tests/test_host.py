@@ -5,7 +5,6 @@ import pytest
 
 from paper_2511_19493_b200 import distributed as D
 from paper_2511_19493_b200 import proximity as P
-from paper_2511_19493_b200.device import relayout_siblings
 from paper_2511_19493_b200.errors import BudgetError, DataError
 
 
@@ -73,25 +72,91 @@ def test_full_triangle_accessors():
     assert ft.to_dense()[1, 0] == 0.5
 
 
-def _descend(st, sv, th, lf, rt, x):
+def host_pack(trees, p, col_cat, layout):
+    """Call the C++ host packer (rfxc_forest_pack_host) — no GPU needed."""
+    import ctypes
+    from paper_2511_19493_b200 import _lib
+    B = len(trees)
+    keep, tabs = [], []
+    for name, dt in (("status", np.int8), ("split_var", np.int32), ("threshold", np.float64),
+                     ("cat_mask", np.int64), ("left", np.int32), ("right", np.int32)):
+        arrs = [np.ascontiguousarray(getattr(t, name), dtype=dt) for t in trees]
+        keep += arrs
+        tabs.append(np.array([a.ctypes.data for a in arrs], dtype=np.uintp))
+    counts = np.array([len(t.status) for t in trees], dtype=np.int64)
+    rec = 8 if layout == _lib.NODES_F32 else 16
+    out = np.zeros(int(counts.sum()) * rec, dtype=np.uint8)
+    off = np.empty(B + 1, np.int64)
+    lc = np.empty(B, np.int32)
+    cc = np.ascontiguousarray(col_cat, dtype=np.uint8)
+    P = ctypes.c_void_p
+    _lib.call("rfxc_forest_pack_host", *(t.ctypes.data_as(P) for t in tabs),
+              counts.ctypes.data_as(P), B, cc.ctypes.data_as(P), p, layout,
+              out.ctypes.data_as(P), off.ctypes.data_as(P), lc.ctypes.data_as(P), 2)
+    return out, off, lc
+
+
+def walk_f32(rec, off, b, x, p):
+    """Decode the 8-byte records and descend (mirror of traverse_kernel)."""
+    from paper_2511_19493_b200.device import feature_bits
+    fb = feature_bits(p)
+    words = rec.view(np.uint32).reshape(-1, 2)
     node = 0
-    while st[node] == 0:
-        node = lf[node] if x[sv[node]] <= th[node] else (rt[node] if rt is not None
-                                                           else lf[node] + 1)
-    return node
+    while True:
+        w0, w1 = int(words[off[b] + node, 0]), int(words[off[b] + node, 1])
+        if w1 == 0:
+            return w0
+        f, cat, left = w1 & ((1 << fb) - 1), (w1 >> fb) & 1, w1 >> (fb + 1)
+        v = np.float32(x[f])
+        if cat:
+            go = ((w0 >> int(v)) & 1) == 1 if int(v) < 32 else False
+        else:
+            go = v <= np.uint32(w0).view(np.float32)
+        node = left + (0 if go else 1)
 
 
-def test_relayout_keeps_routing_and_codes():
+def test_host_packer_relayout_keeps_codes(built):
+    """Hand-built tree with right != left + 1 (tests/test_forest.py:170-185):
+    relaid out breadth-first by the C++ packer, leaf ordinals preserved."""
     from conftest import golden
+    from paper_2511_19493_b200 import _lib
+
+    class T:
+        pass
     h = golden("handbuilt.npz")
-    st, sv, th, cm, lf, order = relayout_siblings(h["status"], h["split_var"], h["threshold"],
-                                                  np.zeros(7, np.int64), h["left"], h["right"])
-    internal = st == 0
-    assert np.all(lf[internal] >= 1)
-    ref_code = np.cumsum(h["status"] == 1) - 1
+    t = T()
+    t.status, t.split_var, t.threshold = h["status"], h["split_var"], h["threshold"]
+    t.cat_mask, t.left, t.right = np.zeros(7, np.int64), h["left"], h["right"]
+    rec, off, lc = host_pack([t], 2, np.zeros(2), _lib.NODES_F32)
+    assert lc[0] == 4
     for x, want in zip(h["points"], h["codes"]):
-        node = _descend(st, sv, th, lf, None, x)
-        assert ref_code[order[node]] == want
+        assert walk_f32(rec, off, 0, x, 2) == want
+
+
+def test_host_packer_matches_oracle_on_trained_forest(orc, mixed):
+    """8-byte records + round-down thresholds route every sample like the
+    reference (categorical masks included) when the values are f32-exact."""
+    from paper_2511_19493_b200 import _lib
+    ds, forest = mixed
+    X = ds.values.astype(np.float32).astype(np.float64)  # make f32-exact copy
+    codes, lc_ref = orc.leaf_membership(forest.trees, forest.col_cat, X)
+    rec, off, lc = host_pack(forest.trees, ds.p, forest.col_cat, _lib.NODES_F32)
+    assert np.array_equal(lc, lc_ref)
+    for i in range(0, ds.n, 7):
+        for b in range(0, forest.ntree, 3):
+            assert walk_f32(rec, off, b, X[i], ds.p) == codes[i, b]
+
+
+def test_values_to_f32_host_exactness(built):
+    import ctypes
+    from paper_2511_19493_b200 import _lib
+    P = ctypes.c_void_p
+    for vals, want in ((np.array([1.5, -2.25, 3.0]), 1), (np.array([0.1, 1.0]), 0)):
+        out = np.empty(len(vals), np.float32)
+        ex = np.zeros(1, np.int32)
+        _lib.call("rfxc_values_to_f32_host", vals.ctypes.data_as(P), len(vals),
+                  out.ctypes.data_as(P), ex.ctypes.data_as(P), 2)
+        assert ex[0] == want and np.array_equal(out, vals.astype(np.float32))
 
 
 def test_tree_and_row_shards_cover_exactly():
