@@ -20,10 +20,13 @@
 //
 // Layout: one CTA per SM (cooperative launch); CTA c owns a contiguous row
 // slice and keeps that slice of the factor resident in shared memory for the
-// whole run (f64 rows, or int8 codes x per-column scales for large n; the
-// global-memory path is the fallback).  Every reduction has a fixed order
-// (register tiles -> fixed smem combine -> fixed block order), so results
-// are bit-reproducible and every stopping decision is identical in every CTA.
+// whole run (f64 rows, or int8 codes x per-column scales for large n, odd
+// row stride so lane-per-row reads are conflict-free; global memory is the
+// fallback).  The kernel is templated on that storage so the inner loops are
+// branch-free.  Every reduction has a fixed order (register tiles -> fixed
+// smem combine -> fixed block order), so results are bit-reproducible and
+// every stopping decision is identical in every CTA.  The work is FP64-FMA
+// bound: per matvec and row, ~r(r+1)/2 FMAs in each of the two passes.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -36,6 +39,7 @@ constexpr int MT = 512;             // threads per CTA
 constexpr int MW = MT / 32;         // warps per CTA
 constexpr int SLOTS = 24;           // small-reduction slots per CTA
 constexpr int SMEM_BUDGET = 220 * 1024;
+constexpr int RMAX_REG = 32;        // rows held in registers for r <= 32
 
 enum { QS_F64 = 0, QS_I8 = 1, QS_GLOBAL = 2 };
 
@@ -51,7 +55,6 @@ struct MdsArgs {
     double tol;
     int mode;               // 0: MDS, 1: one gram_matvec of V[0] into w
     int qs;                 // QS_* storage of the factor slice
-    int s_in_smem;          // S' (r+1)^2 in shared memory
     int64_t rpb;            // rows per CTA
     double* V;              // k x n: start vectors in, found vectors out
     double* w;              // n
@@ -59,7 +62,6 @@ struct MdsArgs {
     double* sparts;         // grid x (E + 8) (S' partials + deflation dots)
     double* tot;            // E + 8: totals of the current matvec
     double* cst;            // E: constants Q'^T Q' (G = Q^T Q, c = Q^T 1, n)
-    double* Sg;             // grid x (r+1)^2 expanded S' (global fallback)
     double* coords;         // n x k
     double* info;           // k x 4
     int32_t* k_used;
@@ -78,6 +80,10 @@ __host__ __device__ __forceinline__ int nentry(int r)
 {
     const int t = ntile(r);
     return 16 * t * (t + 1) / 2;
+}
+__host__ __device__ __forceinline__ int tile_index(int ta, int tb, int T)
+{
+    return ta * T - ta * (ta - 1) / 2 + (tb - ta);  // ta <= tb
 }
 
 // ---------------------------------------------------------------- reductions
@@ -178,61 +184,69 @@ __device__ int64_t grid_argmax_abs(Ctx& C, const MdsArgs& A, const double* x)
 }
 
 // ------------------------------------------------------------- factor rows
+// Factor slice accessor; QSM fixed at compile time (no per-element branch).
+template <int QSM>
 struct Rows {
-    int qs;
     int r;
-    const double* f64;   // smem (QS_F64) or global (QS_GLOBAL), row stride r
-    const int8_t* i8;    // smem (QS_I8), row stride r
+    int ld;              // row stride (odd for the shared-memory layouts)
+    const double* f64;   // smem slice (QS_F64) or global dq (QS_GLOBAL)
+    const int8_t* i8;    // smem codes (QS_I8)
     const double* sc;    // smem scales (QS_I8)
-    int64_t base;        // first global row of the slice (QS_GLOBAL indexing)
+    int64_t base;        // first global row of the slice (QS_GLOBAL)
 
-    // q'_{row, col} of the augmented factor [Q | 1 | 0 ...]; row is slice-local
-    __device__ __forceinline__ double q(int64_t row, int col) const
+    __device__ __forceinline__ double q(int64_t row, int col) const  // col < r
     {
-        if (col < r) {
-            if (qs == QS_I8) return (double)i8[row * r + col] * sc[col];
-            if (qs == QS_F64) return f64[row * r + col];
-            return __ldg(f64 + (base + row) * r + col);
-        }
-        return col == r ? 1.0 : 0.0;
+        if (QSM == QS_I8) return (double)i8[row * ld + col] * sc[col];
+        if (QSM == QS_F64) return f64[row * ld + col];
+        return __ldg(f64 + (base + row) * r + col);
     }
 };
 
-__host__ __device__ __forceinline__ int tile_index(int ta, int tb, int T)
+// S' partial of this CTA: sum over slice rows of u_i q'_i q'_i^T (q' = [q | 1])
+// as 4x4 register tiles of the upper triangle; row groups split the slice
+// and are combined in a fixed order.  Writes nentry(r) values to `out`.
+template <int QSM>
+__device__ __forceinline__ void tile_rows(const Rows<QSM>& Q, int ta, int tb, int r,
+                                          const double* us, int64_t i0, int64_t rows,
+                                          int64_t step, double* acc)
 {
-    return ta * T - ta * (ta - 1) / 2 + (tb - ta);  // ta <= tb
+    bool va[4], vb[4];
+#pragma unroll
+    for (int x = 0; x < 4; x++) {
+        va[x] = 4 * ta + x < r;
+        vb[x] = 4 * tb + x < r;
+    }
+    for (int64_t i = i0; i < rows; i += step) {
+        const double u = us[i];
+        double qa[4], qb[4];
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+            const int ca = 4 * ta + x, cb = 4 * tb + x;
+            qa[x] = u * (va[x] ? Q.q(i, ca) : (ca == r ? 1.0 : 0.0));
+            qb[x] = vb[x] ? Q.q(i, cb) : (cb == r ? 1.0 : 0.0);
+        }
+#pragma unroll
+        for (int x = 0; x < 4; x++)
+#pragma unroll
+            for (int y = 0; y < 4; y++) acc[4 * x + y] += qa[x] * qb[y];
+    }
 }
 
-// S' partial of this CTA: sum over slice rows of u_i q'_i q'_i^T as 4x4
-// register tiles of the upper triangle; row groups split the slice and are
-// combined in a fixed order.  Writes nentry(r) values to `out`.
-__device__ void spass(const Rows& Q, const double* us, int64_t rows, double* out,
+template <int QSM>
+__device__ void spass(const Rows<QSM>& Q, const double* us, int64_t rows, double* out,
                       double* scratch)
 {
-    const int T = ntile(Q.r);
+    const int r = Q.r, T = ntile(r);
     const int tiles = T * (T + 1) / 2;
     const int tid = threadIdx.x;
+    double acc[16];
     if (tiles > MT) {  // large r: every thread owns whole tiles, all rows
         for (int tile = tid; tile < tiles; tile += MT) {
             int ta = 0, rem = tile;
             while (rem >= T - ta) { rem -= T - ta; ta++; }
-            const int tb = ta + rem;
-            double acc[16];
 #pragma unroll
             for (int e = 0; e < 16; e++) acc[e] = 0.0;
-            for (int64_t i = 0; i < rows; i++) {
-                const double u = us[i];
-                double qa[4], qb[4];
-#pragma unroll
-                for (int x = 0; x < 4; x++) {
-                    qa[x] = u * Q.q(i, 4 * ta + x);
-                    qb[x] = Q.q(i, 4 * tb + x);
-                }
-#pragma unroll
-                for (int x = 0; x < 4; x++)
-#pragma unroll
-                    for (int y = 0; y < 4; y++) acc[4 * x + y] += qa[x] * qb[y];
-            }
+            tile_rows(Q, ta, ta + rem, r, us, 0, rows, 1, acc);
 #pragma unroll
             for (int e = 0; e < 16; e++) out[tile * 16 + e] = acc[e];
         }
@@ -241,28 +255,12 @@ __device__ void spass(const Rows& Q, const double* us, int64_t rows, double* out
     }
     const int groups = MT / tiles;
     const int g = tid / tiles, tile = tid % tiles;
-    double acc[16];
 #pragma unroll
     for (int e = 0; e < 16; e++) acc[e] = 0.0;
     int ta = 0, rem = tile;
     while (rem >= T - ta) { rem -= T - ta; ta++; }
-    const int tb = ta + rem;
     for (int tt = tid; tt < tiles * 16; tt += MT) scratch[tt] = 0.0;
-    if (g < groups) {
-        for (int64_t i = g; i < rows; i += groups) {
-            const double u = us[i];
-            double qa[4], qb[4];
-#pragma unroll
-            for (int x = 0; x < 4; x++) {
-                qa[x] = u * Q.q(i, 4 * ta + x);
-                qb[x] = Q.q(i, 4 * tb + x);
-            }
-#pragma unroll
-            for (int x = 0; x < 4; x++)
-#pragma unroll
-                for (int y = 0; y < 4; y++) acc[4 * x + y] += qa[x] * qb[y];
-        }
-    }
+    if (g < groups) tile_rows(Q, ta, ta + rem, r, us, g, rows, groups, acc);
     __syncthreads();
     for (int gg = 0; gg < groups; gg++) {  // fixed combine order
         if (g == gg) {
@@ -283,10 +281,34 @@ __device__ __forceinline__ double sprime(const double* tot, int a, int b, int T)
     return tot[16 * tile_index(ta, tb, T) + 4 * x + y];
 }
 
+// Row pass, lane per row with the row in registers (r <= R): returns
+// pu = q.t and ppu = q^T S q for slice row i.  S is symmetric (R x R,
+// zero-padded, broadcast from shared memory), t = S'[:, r].
+template <int QSM, int R>
+__device__ __forceinline__ void row_terms_reg(const Rows<QSM>& Q, int64_t i, bool valid,
+                                              const double* Sp, const double* tv, double& pu,
+                                              double& ppu)
+{
+    double q[R];
+#pragma unroll
+    for (int b = 0; b < R; b++) q[b] = (valid && b < Q.r) ? Q.q(i, b) : 0.0;
+    pu = 0.0;
+    ppu = 0.0;
+#pragma unroll
+    for (int a = 0; a < R; a++) {
+        double acc = 0.0;
+#pragma unroll
+        for (int b = a + 1; b < R; b++) acc += Sp[a * R + b] * q[b];
+        ppu += q[a] * (Sp[a * R + a] * q[a] + 2.0 * acc);
+        pu += q[a] * tv[a];
+    }
+}
+
 // y = G x - sum_{f<nf} lam_f (v_f . x) v_f   (deflated_matvec, mds.py:203-207)
 // sx: sum of x over all rows.  Two grid barriers.
-__device__ void matvec(Ctx& C, const MdsArgs& A, const Rows& Q, const double* x, double sx,
-                       double* y, int nf, const double* lam, double* Ssm, double* us,
+template <int QSM>
+__device__ void matvec(Ctx& C, const MdsArgs& A, const Rows<QSM>& Q, const double* x, double sx,
+                       double* y, int nf, const double* lam, double* Sp, double* tv, double* us,
                        double* scratch)
 {
     const int r = A.r, T = ntile(r), E = nentry(r);
@@ -317,36 +339,49 @@ __device__ void matvec(Ctx& C, const MdsArgs& A, const Rows& Q, const double* x,
         }
     }
     C.grid.sync();
-    const int ra = r + 1;
-    double* S = A.s_in_smem ? Ssm : A.Sg + (int64_t)blockIdx.x * ra * ra;
-    for (int e = threadIdx.x; e < ra * ra; e += MT) S[e] = sprime(A.tot, e / ra, e % ra, T);
+    // padded symmetric S (RP x RP) and t into shared memory
+    const int RP = r <= 16 ? 16 : (r <= RMAX_REG ? RMAX_REG : r);
+    for (int e = threadIdx.x; e < RP * RP; e += MT) {
+        const int a = e / RP, b = e % RP;
+        Sp[e] = (a < r && b < r) ? sprime(A.tot, a, b, T) : 0.0;
+    }
+    for (int a = threadIdx.x; a < RP; a += MT) tv[a] = a < r ? sprime(A.tot, a, r, T) : 0.0;
     __syncthreads();
-    const double su = S[r * ra + r];
+    const double su = sprime(A.tot, r, r, T);
     const double pm = A.pmax;
-    double ct, sgm;  // c.t and <S, G>
+    double ct, sgm;  // c.t and <S, G> -> closed-form mean of z
     {
         double a = 0.0, b = 0.0;
         for (int e = threadIdx.x; e < r * r; e += MT)
-            b += S[(e / r) * ra + (e % r)] * sprime(A.cst, e / r, e % r, T);
-        for (int aa = threadIdx.x; aa < r; aa += MT) a += sprime(A.cst, aa, r, T) * S[aa * ra + r];
+            b += Sp[(e / r) * RP + (e % r)] * sprime(A.cst, e / r, e % r, T);
+        for (int aa = threadIdx.x; aa < r; aa += MT) a += sprime(A.cst, aa, r, T) * tv[aa];
         ct = block_sum(a, C.red);
         sgm = block_sum(b, C.red);
     }
     const double mz = (pm * pm) * su - 2.0 * pm * ct / (double)n + sgm / (double)n;
     const double* d = A.tot + E;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t i = warp; i < rows; i += MW) {
-        double pu = 0.0, ppu = 0.0;
-        for (int a = lane; a < r; a += 32) {
-            double sa = 0.0;
-            for (int b = 0; b < r; b++) sa += S[b * ra + a] * Q.q(i, b);
-            const double qa = Q.q(i, a);
-            ppu += qa * sa;
-            pu += qa * S[a * ra + r];
+    for (int64_t i0 = 0; i0 < rows; i0 += MT) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool valid = i < rows;
+        double pu, ppu;
+        if (r <= 16) {
+            row_terms_reg<QSM, 16>(Q, i, valid, Sp, tv, pu, ppu);
+        } else if (r <= RMAX_REG) {
+            row_terms_reg<QSM, RMAX_REG>(Q, i, valid, Sp, tv, pu, ppu);
+        } else {  // generic: S from shared memory, row from the slice
+            pu = 0.0;
+            ppu = 0.0;
+            if (valid) {
+                for (int a = 0; a < r; a++) {
+                    const double qa = Q.q(i, a);
+                    double acc = 0.0;
+                    for (int b = a + 1; b < r; b++) acc += Sp[a * RP + b] * Q.q(i, b);
+                    ppu += qa * (Sp[a * RP + a] * qa + 2.0 * acc);
+                    pu += qa * tv[a];
+                }
+            }
         }
-        pu = warp_sum(pu);
-        ppu = warp_sum(ppu);
-        if (lane == 0) {
+        if (valid) {
             const double zi = (pm * pm) * su - 2.0 * pm * pu + ppu;
             double yi = -0.5 * (zi - mz);
             for (int f = 0; f < nf; f++) yi -= lam[f] * d[f] * A.V[(int64_t)f * n + C.r0 + i];
@@ -356,34 +391,39 @@ __device__ void matvec(Ctx& C, const MdsArgs& A, const Rows& Q, const double* x,
     __syncthreads();
 }
 
+template <int QSM>
 __global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
 {
     extern __shared__ __align__(16) unsigned char msm[];
     __shared__ double red[32];
     __shared__ double bcast[SLOTS];
     __shared__ double lam_s[8];
-    const int r = A.r, ra = r + 1, T = ntile(r), E = nentry(r);
+    const int r = A.r, T = ntile(r), E = nentry(r);
+    const int RP = r <= 16 ? 16 : (r <= RMAX_REG ? RMAX_REG : r);
     Ctx C{cg::this_grid(), 0, 0, 0, red, bcast};
     const int64_t n = A.n;
     C.r0 = min64(n, blockIdx.x * A.rpb);
     C.r1 = min64(n, C.r0 + A.rpb);
     const int64_t rows = C.r1 - C.r0;
 
-    // shared memory: [S'] [tile scratch] [u] [factor slice]
-    double* Ssm = reinterpret_cast<double*>(msm);
-    double* scratch = Ssm + (A.s_in_smem ? ra * ra : 0);
+    // shared memory: [S RPxRP] [t RP] [tile scratch] [u rpb] [factor slice]
+    double* Sp = reinterpret_cast<double*>(msm);
+    double* tv = Sp + RP * RP;
+    double* scratch = tv + RP;
     double* us = scratch + 16 * T * (T + 1) / 2;
     unsigned char* qbase = reinterpret_cast<unsigned char*>(us + A.rpb);
-    Rows Q{A.qs, r, nullptr, nullptr, nullptr, C.r0};
-    if (A.qs == QS_F64) {
+    Rows<QSM> Q{r, r | 1, nullptr, nullptr, nullptr, C.r0};
+    if (QSM == QS_F64) {
         double* qs = reinterpret_cast<double*>(qbase);
-        for (int64_t e = threadIdx.x; e < rows * r; e += MT) qs[e] = A.dq[C.r0 * r + e];
+        for (int64_t e = threadIdx.x; e < rows * r; e += MT)
+            qs[(e / r) * Q.ld + e % r] = A.dq[C.r0 * r + e];
         Q.f64 = qs;
-    } else if (A.qs == QS_I8) {
+    } else if (QSM == QS_I8) {
         double* sc = reinterpret_cast<double*>(qbase);
         int8_t* qs = reinterpret_cast<int8_t*>(sc + r);
         for (int e = threadIdx.x; e < r; e += MT) sc[e] = A.scales[e];
-        for (int64_t e = threadIdx.x; e < rows * r; e += MT) qs[e] = A.codes[C.r0 * r + e];
+        for (int64_t e = threadIdx.x; e < rows * r; e += MT)
+            qs[(e / r) * Q.ld + e % r] = A.codes[C.r0 * r + e];
         Q.i8 = qs;
         Q.sc = sc;
     } else {
@@ -413,7 +453,7 @@ __global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
         double s[1] = {0.0};
         for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) s[0] += A.V[i];
         grid_sum(C, A, s, 1);
-        matvec(C, A, Q, A.V, s[0], A.w, 0, lam_s, Ssm, us, scratch);
+        matvec(C, A, Q, A.V, s[0], A.w, 0, lam_s, Sp, tv, us, scratch);
         return;
     }
 
@@ -445,7 +485,7 @@ __global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
         bool conv = false;
         int it = 0;
         for (it = 1; it <= A.max_it; it++) {
-            matvec(C, A, Q, v, sumv, A.w, comp, lam_s, Ssm, us, scratch);
+            matvec(C, A, Q, v, sumv, A.w, comp, lam_s, Sp, tv, us, scratch);
             // all projections in one reduction: e_f = v_f.w, g_f = v_f.v, v.w, w.w
             double dots[2 * 8 + 2];
             const int m = 2 * comp + 2;
@@ -494,7 +534,7 @@ __global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
         }
         if (it > A.max_it) it = A.max_it;
         // residual |deflated_matvec(v) - lam v| / |lam|  (mds.py:241-242)
-        matvec(C, A, Q, v, sumv, A.w, comp, lam_s, Ssm, us, scratch);
+        matvec(C, A, Q, v, sumv, A.w, comp, lam_s, Sp, tv, us, scratch);
         double rr[1] = {0.0};
         for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) {
             const double e = A.w[i] - lam * v[i];
@@ -526,7 +566,7 @@ __global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
 
 // ------------------------------------------------------------------- host
 struct Layout {
-    int64_t V, w, parts, sparts, tot, cst, Sg, bytes;
+    int64_t V, w, parts, sparts, tot, cst, bytes;
 };
 
 static int grid_size() { return sm_count(); }
@@ -548,7 +588,6 @@ static Layout mds_layout(int64_t n, int r, int k)
     L.sparts = take((int64_t)G * (E + 8));
     L.tot = take(E + 8);
     L.cst = take(E + 8);
-    L.Sg = take((int64_t)G * (r + 1) * (r + 1));
     L.bytes = o;
     return L;
 }
@@ -556,25 +595,41 @@ static Layout mds_layout(int64_t n, int r, int k)
 // choose the factor storage; returns the dynamic shared memory size
 static size_t plan_smem(MdsArgs& A)
 {
-    const int r = A.r, ra = r + 1;
+    const int r = A.r;
     const int64_t T = ntile(r);
+    const int RP = r <= 16 ? 16 : (r <= RMAX_REG ? RMAX_REG : r);
+    const int ld = r | 1;
     A.rpb = (A.n + grid_size() - 1) / grid_size();
-    const size_t s_bytes = (size_t)ra * ra * 8;
-    const size_t fixed = (size_t)(16 * T * (T + 1) / 2) * 8 + (size_t)A.rpb * 8;
-    const size_t f64_rows = (size_t)A.rpb * r * 8, i8_rows = (size_t)r * 8 + (size_t)A.rpb * r;
-    A.s_in_smem = s_bytes + fixed + i8_rows <= SMEM_BUDGET;
-    const size_t sb = A.s_in_smem ? s_bytes : 0;
-    if (sb + fixed + f64_rows <= SMEM_BUDGET) {
+    const size_t fixed = ((size_t)RP * RP + RP + 16 * T * (T + 1) / 2 + (size_t)A.rpb) * 8;
+    const size_t f64_rows = (size_t)A.rpb * ld * 8;
+    const size_t i8_rows = (size_t)r * 8 + (size_t)A.rpb * ld;
+    if (fixed + f64_rows <= SMEM_BUDGET) {
         A.qs = QS_F64;
-        return sb + fixed + f64_rows;
+        return fixed + f64_rows;
     }
-    if (A.codes && sb + fixed + i8_rows <= SMEM_BUDGET) {
+    if (A.codes && fixed + i8_rows <= SMEM_BUDGET) {
         A.qs = QS_I8;
-        return sb + fixed + i8_rows;
+        return fixed + i8_rows;
     }
     A.qs = QS_GLOBAL;
-    if (sb + fixed > SMEM_BUDGET) A.s_in_smem = 0;
-    return (A.s_in_smem ? s_bytes : 0) + fixed;
+    return fixed;
+}
+
+template <int QSM>
+static int launch_q(MdsArgs& A, size_t smem, cudaStream_t st)
+{
+    auto kern = mds_kernel<QSM>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(smem, 1));
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "mds attr: %s", cudaGetErrorString(e));
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, MT, smem);
+    if (occ < 1) return fail(RFXC_ERUNTIME, "mds: kernel does not fit an SM (r=%d)", A.r);
+    void* args[] = {&A};
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid_size()), dim3(MT), args, smem,
+                                    st);
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "mds launch: %s", cudaGetErrorString(e));
+    return check_launch("mds");
 }
 
 static int launch_mds(MdsArgs& A, cudaStream_t st)
@@ -582,17 +637,9 @@ static int launch_mds(MdsArgs& A, cudaStream_t st)
     const size_t smem = plan_smem(A);
     if (smem > SMEM_BUDGET)
         return fail(RFXC_EDATA, "mds: n=%lld r=%d too large for one GPU", (long long)A.n, A.r);
-    cudaError_t e = cudaFuncSetAttribute(mds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)std::max<size_t>(smem, 1));
-    if (e != cudaSuccess) return fail(RFXC_ECUDA, "mds attr: %s", cudaGetErrorString(e));
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mds_kernel, MT, smem);
-    if (occ < 1) return fail(RFXC_ERUNTIME, "mds: kernel does not fit an SM (r=%d)", A.r);
-    void* args[] = {&A};
-    e = cudaLaunchCooperativeKernel((const void*)mds_kernel, dim3(grid_size()), dim3(MT), args,
-                                    smem, st);
-    if (e != cudaSuccess) return fail(RFXC_ECUDA, "mds launch: %s", cudaGetErrorString(e));
-    return check_launch("mds");
+    if (A.qs == QS_F64) return launch_q<QS_F64>(A, smem, st);
+    if (A.qs == QS_I8) return launch_q<QS_I8>(A, smem, st);
+    return launch_q<QS_GLOBAL>(A, smem, st);
 }
 
 static void bind(MdsArgs& A, const Layout& L, void* d_work)
@@ -604,7 +651,6 @@ static void bind(MdsArgs& A, const Layout& L, void* d_work)
     A.sparts = reinterpret_cast<double*>(base + L.sparts);
     A.tot = reinterpret_cast<double*>(base + L.tot);
     A.cst = reinterpret_cast<double*>(base + L.cst);
-    A.Sg = reinterpret_cast<double*>(base + L.Sg);
 }
 
 }  // namespace rfxc

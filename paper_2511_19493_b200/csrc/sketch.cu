@@ -191,44 +191,65 @@ __global__ void __launch_bounds__(GRAM_THREADS)
 gram_partial_kernel(const double* __restrict__ A, int lda, const double* __restrict__ Bm, int ldb,
                     int64_t n, int ka, int kb, int64_t rows_per_part, double* __restrict__ parts)
 {
-    extern __shared__ double gsm[];
-    double* As = gsm;                       // GRAM_ROWS x ka
-    double* Bs = gsm + GRAM_ROWS * ka;      // GRAM_ROWS x kb
+    // 4x4 register tiles of C over (ka x kb); row groups split this part's rows
+    // and are combined in a fixed order through shared memory.
+    extern __shared__ double gsm[];  // tiles x 16
     const int64_t r0 = blockIdx.x * rows_per_part;
     const int64_t r1 = min64(n, r0 + rows_per_part);
-    const int E = ka * kb;
-    constexpr int MAXE = 64;  // entries per thread (ka*kb <= 64*256 per launch)
-    double acc[MAXE];
+    const int TA = (ka + 3) / 4, TB = (kb + 3) / 4, tiles = TA * TB;
+    const int groups = max(1, GRAM_THREADS / tiles);
+    const int tid = threadIdx.x;
+    const int g = tid / tiles;
+    for (int e = tid; e < tiles * 16; e += GRAM_THREADS) gsm[e] = 0.0;
+    __syncthreads();
+    for (int tile0 = 0; tile0 < tiles; tile0 += GRAM_THREADS) {
+        const int tile = tiles > GRAM_THREADS ? tile0 + tid : tid % tiles;
+        const bool active = tile < tiles && g < groups;
+        double acc[16];
 #pragma unroll
-    for (int q = 0; q < MAXE; q++) acc[q] = 0.0;
-    for (int64_t base = r0; base < r1; base += GRAM_ROWS) {
-        const int m = (int)min64(GRAM_ROWS, r1 - base);
-        for (int e = threadIdx.x; e < GRAM_ROWS * ka; e += GRAM_THREADS) {
-            const int r = e / ka;
-            As[e] = r < m ? A[(base + r) * lda + e % ka] : 0.0;
-        }
-        for (int e = threadIdx.x; e < GRAM_ROWS * kb; e += GRAM_THREADS) {
-            const int r = e / kb;
-            Bs[e] = r < m ? Bm[(base + r) * ldb + e % kb] : 0.0;
-        }
-        __syncthreads();
+        for (int e = 0; e < 16; e++) acc[e] = 0.0;
+        const int ta = tile / TB, tb = tile % TB;
+        if (active) {
+            bool va[4], vb[4];
 #pragma unroll
-        for (int q = 0; q < MAXE; q++) {
-            const int e = threadIdx.x + q * GRAM_THREADS;
-            if (e < E) {
-                const int a = e / kb, b = e % kb;
-                double s = acc[q];
-                for (int r = 0; r < m; r++) s += As[r * ka + a] * Bs[r * kb + b];
-                acc[q] = s;
+            for (int x = 0; x < 4; x++) {
+                va[x] = 4 * ta + x < ka;
+                vb[x] = 4 * tb + x < kb;
+            }
+            const int gstep = tiles > GRAM_THREADS ? 1 : groups;
+            const int gi = tiles > GRAM_THREADS ? 0 : g;
+            for (int64_t i = r0 + gi; i < r1; i += gstep) {
+                double qa[4], qb[4];
+#pragma unroll
+                for (int x = 0; x < 4; x++) {
+                    qa[x] = va[x] ? __ldg(A + i * lda + 4 * ta + x) : 0.0;
+                    qb[x] = vb[x] ? __ldg(Bm + i * ldb + 4 * tb + x) : 0.0;
+                }
+#pragma unroll
+                for (int x = 0; x < 4; x++)
+#pragma unroll
+                    for (int y = 0; y < 4; y++) acc[4 * x + y] += qa[x] * qb[y];
             }
         }
-        __syncthreads();
-    }
-    double* out = parts + (int64_t)blockIdx.x * E;
+        if (tiles > GRAM_THREADS) {
+            if (active)
 #pragma unroll
-    for (int q = 0; q < MAXE; q++) {
-        const int e = threadIdx.x + q * GRAM_THREADS;
-        if (e < E) out[e] = acc[q];
+                for (int e = 0; e < 16; e++) gsm[tile * 16 + e] = acc[e];
+        } else {
+            for (int gg = 0; gg < groups; gg++) {  // fixed combine order
+                if (g == gg && active)
+#pragma unroll
+                    for (int e = 0; e < 16; e++) gsm[tile * 16 + e] += acc[e];
+                __syncthreads();
+            }
+        }
+        if (tiles <= GRAM_THREADS) break;
+    }
+    __syncthreads();
+    double* out = parts + (int64_t)blockIdx.x * ka * kb;
+    for (int e = tid; e < ka * kb; e += GRAM_THREADS) {
+        const int a = e / kb, b = e % kb;
+        out[e] = gsm[((a >> 2) * TB + (b >> 2)) * 16 + 4 * (a & 3) + (b & 3)];
     }
 }
 
@@ -335,10 +356,12 @@ extern "C" int rfxc_gram(const double* d_A, const double* d_B, int64_t n, int32_
     cudaStream_t st = as_stream(stream);
     const int parts = gram_parts(n);
     const int64_t rpp = ceil_div(n, parts);
-    const int kbc = std::max(1, std::min<int>(kb, 64 * GRAM_THREADS / ka));  // columns per launch
+    // columns per launch: at most 768 4x4 tiles (96 KB of tile accumulators)
+    const int TA = (ka + 3) / 4;
+    const int kbc = std::max(4, std::min<int>((kb + 3) / 4 * 4, 4 * (768 / TA)));
     for (int c0 = 0; c0 < kb; c0 += kbc) {
         const int w = std::min(kbc, kb - c0);
-        const size_t smem = (size_t)GRAM_ROWS * (ka + w) * 8;
+        const size_t smem = (size_t)TA * ((w + 3) / 4) * 16 * 8;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(gram_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
