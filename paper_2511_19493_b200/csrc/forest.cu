@@ -115,11 +115,12 @@ __global__ void pack_kernel(const int8_t* __restrict__ status,
 }
 
 // ------------------------------------------------------------ K1 traverse
-constexpr int TRAV_T = 128;   // samples per CTA (one per thread)
-constexpr int TRAV_ILP = 4;   // independent tree chains per thread
+constexpr int TRAV_T = 128;   // samples per CTA (one X row each in shared memory)
+constexpr int TRAV_G = 4;     // tree groups per CTA: TRAV_T * TRAV_G threads share the tile
+constexpr int TRAV_ILP = 2;   // independent tree chains per thread
 
 template <int LAYOUT, bool SMEM_X>
-__global__ void __launch_bounds__(TRAV_T)
+__global__ void __launch_bounds__(TRAV_T * TRAV_G, 3)
 traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ node_off,
                 int fb, int p, int tree_lo, int tree_hi, int trees_per_chunk,
                 const void* __restrict__ values_v, int64_t n,
@@ -129,14 +130,15 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
     extern __shared__ __align__(16) unsigned char smem_raw[];
     V* xs = reinterpret_cast<V*>(smem_raw);
     const V* __restrict__ X = reinterpret_cast<const V*>(values_v);
-    const int t = threadIdx.x;
+    const int t = threadIdx.x % TRAV_T;   // sample within the tile
+    const int grp = threadIdx.x / TRAV_T; // tree group
     const int64_t i0 = (int64_t)blockIdx.x * TRAV_T;
     const int64_t i = i0 + t;
     const bool valid = i < n;
     const int stride = p + 1;  // odd row stride spreads banks
     if (SMEM_X) {
         // coalesced: consecutive threads read consecutive samples of feature f
-        for (int f = 0; f < p; f++) {
+        for (int f = grp; f < p; f += TRAV_G) {
             V v = valid ? X[(int64_t)f * n + i] : V(0);
             xs[t * stride + f] = v;
         }
@@ -147,7 +149,8 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
     if (!valid) return;
     const uint32_t fmask = (1u << fb) - 1u;
 
-    for (int b = b_begin; b < b_end; b += TRAV_ILP) {
+    // group g takes trees b_begin + g*ILP + j*(G*ILP) ... (ILP consecutive trees)
+    for (int b = b_begin + grp * TRAV_ILP; b < b_end; b += TRAV_G * TRAV_ILP) {
         int64_t base[TRAV_ILP];
         uint32_t id[TRAV_ILP];
         int32_t code[TRAV_ILP];
@@ -278,19 +281,23 @@ static int launch_traverse(const void* d_nodes, const int64_t* d_node_off, int p
         if (e != cudaSuccess) return fail(RFXC_ECUDA, "traverse attr: %s", cudaGetErrorString(e));
     }
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TRAV_T, smem);
+    const int threads = TRAV_T * TRAV_G;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
     occ = std::max(occ, 1);
     const int64_t tiles = ceil_div(n, TRAV_T);
     const int nt = tree_hi - tree_lo;
-    // enough CTAs for ~6 waves; every chunk a multiple of the chain count
+    // enough CTAs for ~6 waves; every chunk a multiple of the trees one CTA
+    // walks per step (TRAV_G groups x TRAV_ILP chains)
+    const int step = TRAV_G * TRAV_ILP;
     int64_t want = (int64_t)sm_count() * occ * 6;
-    int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(want, tiles), nt));
+    int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(want, tiles),
+                                                             ceil_div(nt, step)));
     int per = (int)ceil_div(nt, chunks);
-    per = (int)ceil_div(per, TRAV_ILP) * TRAV_ILP;
+    per = (int)ceil_div(per, step) * step;
     chunks = (int)ceil_div(nt, per);
     dim3 grid((unsigned)tiles, (unsigned)chunks);
-    kern<<<grid, TRAV_T, smem, st>>>(d_nodes, d_node_off, feature_bits(p), p, tree_lo, tree_hi,
-                                     per, d_values, n, d_codes_tm);
+    kern<<<grid, threads, smem, st>>>(d_nodes, d_node_off, feature_bits(p), p, tree_lo, tree_hi,
+                                      per, d_values, n, d_codes_tm);
     return check_launch("leaf_codes");
 }
 

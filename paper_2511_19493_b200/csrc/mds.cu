@@ -339,13 +339,17 @@ __device__ void matvec(Ctx& C, const MdsArgs& A, const Rows<QSM>& Q, const doubl
         }
     }
     C.grid.sync();
-    // padded symmetric S (RP x RP) and t into shared memory
-    const int RP = r <= 16 ? 16 : (r <= RMAX_REG ? RMAX_REG : r);
-    for (int e = threadIdx.x; e < RP * RP; e += MT) {
-        const int a = e / RP, b = e % RP;
-        Sp[e] = (a < r && b < r) ? sprime(A.tot, a, b, T) : 0.0;
+    // r <= 32: padded symmetric S (RP x RP) and t in shared memory; larger r
+    // reads S' straight from the (L2-resident) totals
+    const bool small = r <= RMAX_REG;
+    const int RP = r <= 16 ? 16 : RMAX_REG;
+    if (small) {
+        for (int e = threadIdx.x; e < RP * RP; e += MT) {
+            const int a = e / RP, b = e % RP;
+            Sp[e] = (a < r && b < r) ? sprime(A.tot, a, b, T) : 0.0;
+        }
+        for (int a = threadIdx.x; a < RP; a += MT) tv[a] = a < r ? sprime(A.tot, a, r, T) : 0.0;
     }
-    for (int a = threadIdx.x; a < RP; a += MT) tv[a] = a < r ? sprime(A.tot, a, r, T) : 0.0;
     __syncthreads();
     const double su = sprime(A.tot, r, r, T);
     const double pm = A.pmax;
@@ -353,8 +357,9 @@ __device__ void matvec(Ctx& C, const MdsArgs& A, const Rows<QSM>& Q, const doubl
     {
         double a = 0.0, b = 0.0;
         for (int e = threadIdx.x; e < r * r; e += MT)
-            b += Sp[(e / r) * RP + (e % r)] * sprime(A.cst, e / r, e % r, T);
-        for (int aa = threadIdx.x; aa < r; aa += MT) a += sprime(A.cst, aa, r, T) * tv[aa];
+            b += sprime(A.tot, e / r, e % r, T) * sprime(A.cst, e / r, e % r, T);
+        for (int aa = threadIdx.x; aa < r; aa += MT)
+            a += sprime(A.cst, aa, r, T) * sprime(A.tot, aa, r, T);
         ct = block_sum(a, C.red);
         sgm = block_sum(b, C.red);
     }
@@ -368,16 +373,16 @@ __device__ void matvec(Ctx& C, const MdsArgs& A, const Rows<QSM>& Q, const doubl
             row_terms_reg<QSM, 16>(Q, i, valid, Sp, tv, pu, ppu);
         } else if (r <= RMAX_REG) {
             row_terms_reg<QSM, RMAX_REG>(Q, i, valid, Sp, tv, pu, ppu);
-        } else {  // generic: S from shared memory, row from the slice
+        } else {  // generic: S' from the totals (L1/L2), row from the slice
             pu = 0.0;
             ppu = 0.0;
             if (valid) {
                 for (int a = 0; a < r; a++) {
                     const double qa = Q.q(i, a);
                     double acc = 0.0;
-                    for (int b = a + 1; b < r; b++) acc += Sp[a * RP + b] * Q.q(i, b);
-                    ppu += qa * (Sp[a * RP + a] * qa + 2.0 * acc);
-                    pu += qa * tv[a];
+                    for (int b = a + 1; b < r; b++) acc += sprime(A.tot, a, b, T) * Q.q(i, b);
+                    ppu += qa * (sprime(A.tot, a, a, T) * qa + 2.0 * acc);
+                    pu += qa * sprime(A.tot, a, r, T);
                 }
             }
         }
@@ -399,7 +404,8 @@ __global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
     __shared__ double bcast[SLOTS];
     __shared__ double lam_s[8];
     const int r = A.r, T = ntile(r), E = nentry(r);
-    const int RP = r <= 16 ? 16 : (r <= RMAX_REG ? RMAX_REG : r);
+    const int RP = r <= 16 ? 16 : (r <= RMAX_REG ? RMAX_REG : 0);
+    const int SCR = T * (T + 1) / 2 <= MT ? 16 * T * (T + 1) / 2 : 0;
     Ctx C{cg::this_grid(), 0, 0, 0, red, bcast};
     const int64_t n = A.n;
     C.r0 = min64(n, blockIdx.x * A.rpb);
@@ -410,7 +416,7 @@ __global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
     double* Sp = reinterpret_cast<double*>(msm);
     double* tv = Sp + RP * RP;
     double* scratch = tv + RP;
-    double* us = scratch + 16 * T * (T + 1) / 2;
+    double* us = scratch + SCR;
     unsigned char* qbase = reinterpret_cast<unsigned char*>(us + A.rpb);
     Rows<QSM> Q{r, r | 1, nullptr, nullptr, nullptr, C.r0};
     if (QSM == QS_F64) {
@@ -597,10 +603,11 @@ static size_t plan_smem(MdsArgs& A)
 {
     const int r = A.r;
     const int64_t T = ntile(r);
-    const int RP = r <= 16 ? 16 : (r <= RMAX_REG ? RMAX_REG : r);
+    const int RP = r <= 16 ? 16 : (r <= RMAX_REG ? RMAX_REG : 0);
+    const int64_t SCR = T * (T + 1) / 2 <= MT ? 16 * T * (T + 1) / 2 : 0;
     const int ld = r | 1;
     A.rpb = (A.n + grid_size() - 1) / grid_size();
-    const size_t fixed = ((size_t)RP * RP + RP + 16 * T * (T + 1) / 2 + (size_t)A.rpb) * 8;
+    const size_t fixed = ((size_t)RP * RP + RP + SCR + (size_t)A.rpb) * 8;
     const size_t f64_rows = (size_t)A.rpb * ld * 8;
     const size_t i8_rows = (size_t)r * 8 + (size_t)A.rpb * ld;
     if (fixed + f64_rows <= SMEM_BUDGET) {

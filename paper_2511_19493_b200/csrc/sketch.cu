@@ -59,7 +59,21 @@ __global__ void pack_f32_kernel(const double* __restrict__ in, int64_t n, int k,
 
 // -------------------------------------------------------------- leaf sums
 // Lanes cover one 32-float4 (128-column) chunk of a row: lane = slot*k4c + c4,
-// R = 32 / k4c rows in flight per warp step.
+// R = 32 / k4c rows per warp step.  Leaves are taken 32 at a time per warp
+// (their run bounds fetched in one coalesced load); a leaf's member ids are
+// fetched 32 at a time (coalesced) and then up to SK_U row loads per lane are
+// issued back to back before any is consumed, so a small leaf costs about
+// two memory round trips instead of one per member.
+constexpr int SK_U = 8;
+
+__device__ __forceinline__ void add4(double& a0, double& a1, double& a2, double& a3, float4 x)
+{
+    a0 += (double)x.x;
+    a1 += (double)x.y;
+    a2 += (double)x.z;
+    a3 += (double)x.w;
+}
+
 __global__ void __launch_bounds__(256)
 leaf_sums_kernel(const int32_t* __restrict__ perm, const int64_t* __restrict__ seg, int64_t g_lo,
                  int64_t g_hi, const float4* __restrict__ X4, int k4, float4* __restrict__ S4)
@@ -67,45 +81,51 @@ leaf_sums_kernel(const int32_t* __restrict__ perm, const int64_t* __restrict__ s
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int cc = 0; cc < k4; cc += 32) {
         const int k4c = min(32, k4 - cc);
         const int R = 32 / k4c;
         const int slot = lane / k4c, c4 = lane % k4c;
         const bool on = slot < R;
-        for (int64_t g = g_lo + warp; g < g_hi; g += nwarps) {
-            const int64_t s = seg[g], e = seg[g + 1];
-            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-            int64_t a = s + slot;
-            // 4 independent rows in flight per lane
-            for (; on && a + 3 * R < e; a += 4 * R) {
-                const int32_t r0 = __ldg(perm + a), r1 = __ldg(perm + a + R);
-                const int32_t r2 = __ldg(perm + a + 2 * R), r3 = __ldg(perm + a + 3 * R);
-                const float4 x0 = __ldg(X4 + (int64_t)r0 * k4 + cc + c4);
-                const float4 x1 = __ldg(X4 + (int64_t)r1 * k4 + cc + c4);
-                const float4 x2 = __ldg(X4 + (int64_t)r2 * k4 + cc + c4);
-                const float4 x3 = __ldg(X4 + (int64_t)r3 * k4 + cc + c4);
-                a0 += (double)x0.x; a1 += (double)x0.y; a2 += (double)x0.z; a3 += (double)x0.w;
-                a0 += (double)x1.x; a1 += (double)x1.y; a2 += (double)x1.z; a3 += (double)x1.w;
-                a0 += (double)x2.x; a1 += (double)x2.y; a2 += (double)x2.z; a3 += (double)x2.w;
-                a0 += (double)x3.x; a1 += (double)x3.y; a2 += (double)x3.z; a3 += (double)x3.w;
+        for (int64_t g0 = g_lo + warp * 32; g0 < g_hi; g0 += nwarps * 32) {
+            const int64_t gj = g0 + lane;
+            int64_t sj = 0, ej = 0;
+            if (gj < g_hi) {
+                sj = seg[gj];
+                ej = seg[gj + 1];
             }
-            for (; on && a < e; a += R) {
-                const int32_t r0 = __ldg(perm + a);
-                const float4 x0 = __ldg(X4 + (int64_t)r0 * k4 + cc + c4);
-                a0 += (double)x0.x; a1 += (double)x0.y; a2 += (double)x0.z; a3 += (double)x0.w;
+            const int nleaf = (int)min64(32, g_hi - g0);
+            for (int jj = 0; jj < nleaf; jj++) {
+                const int64_t s = __shfl_sync(0xffffffffu, sj, jj);
+                const int64_t e = __shfl_sync(0xffffffffu, ej, jj);
+                double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+                for (int64_t base = s; base < e; base += 32) {
+                    const int m = (int)min64(32, e - base);
+                    const int32_t rid = lane < m ? __ldg(perm + base + lane) : 0;
+                    for (int t0 = 0; t0 < m; t0 += R * SK_U) {
+                        float4 x[SK_U];
+#pragma unroll
+                        for (int u = 0; u < SK_U; u++) {
+                            const int t = t0 + u * R + slot;
+                            const int r = __shfl_sync(0xffffffffu, rid, min(t, 31));
+                            x[u] = (on && t < m) ? __ldg(X4 + (int64_t)r * k4 + cc + c4) : z4;
+                        }
+#pragma unroll
+                        for (int u = 0; u < SK_U; u++) add4(a0, a1, a2, a3, x[u]);
+                    }
+                }
+                for (int sl = 1; sl < R; sl++) {
+                    const int src = min(31, lane + sl * k4c);
+                    const double b0 = __shfl_sync(0xffffffffu, a0, src);
+                    const double b1 = __shfl_sync(0xffffffffu, a1, src);
+                    const double b2 = __shfl_sync(0xffffffffu, a2, src);
+                    const double b3 = __shfl_sync(0xffffffffu, a3, src);
+                    if (slot == 0) { a0 += b0; a1 += b1; a2 += b2; a3 += b3; }
+                }
+                if (slot == 0)
+                    S4[(g0 + jj - g_lo) * k4 + cc + c4] =
+                        make_float4((float)a0, (float)a1, (float)a2, (float)a3);
             }
-            if (!on) a0 = a1 = a2 = a3 = 0.0;
-            for (int sl = 1; sl < R; sl++) {
-                const int src = min(31, lane + sl * k4c);
-                const double b0 = __shfl_sync(0xffffffffu, a0, src);
-                const double b1 = __shfl_sync(0xffffffffu, a1, src);
-                const double b2 = __shfl_sync(0xffffffffu, a2, src);
-                const double b3 = __shfl_sync(0xffffffffu, a3, src);
-                if (slot == 0) { a0 += b0; a1 += b1; a2 += b2; a3 += b3; }
-            }
-            if (slot == 0)
-                S4[(g - g_lo) * k4 + cc + c4] = make_float4((float)a0, (float)a1, (float)a2,
-                                                            (float)a3);
         }
     }
 }
@@ -124,35 +144,28 @@ leaf_gather_kernel(const int32_t* __restrict__ codes, int64_t n, int Bl,
         const int R = 32 / k4c;
         const int slot = lane / k4c, c4 = lane % k4c;
         const bool on = slot < R;
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int64_t i = warp; i < n; i += nwarps) {
             const int32_t* row = codes + i * Bl;
             double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            // global leaf ids of this lane's tree in the chunk (next chunk prefetched)
+            int32_t cnext = lane < Bl ? __ldg(row + lane) : 0;
             for (int b0 = 0; b0 < Bl; b0 += 32) {
                 const int bl = b0 + lane;
-                int64_t gl = 0;
-                if (bl < Bl) gl = leaf_base[bl] + (int64_t)__ldg(row + bl);
+                const int32_t code = cnext;
+                if (b0 + 32 + lane < Bl) cnext = __ldg(row + b0 + 32 + lane);
+                const int64_t gl = bl < Bl ? leaf_base[bl] + (int64_t)code : 0;
                 const int nb = min(32, Bl - b0);
-                int t = 0;
-                for (; t + 2 * R <= nb; t += 2 * R) {
-                    const int64_t g0 = __shfl_sync(0xffffffffu, gl, min(31, t + slot));
-                    const int64_t g1 = __shfl_sync(0xffffffffu, gl, min(31, t + R + slot));
-                    if (on) {
-                        const float4 x0 = __ldg(S4 + g0 * k4 + cc + c4);
-                        const float4 x1 = __ldg(S4 + g1 * k4 + cc + c4);
-                        a0 += (double)x0.x; a1 += (double)x0.y;
-                        a2 += (double)x0.z; a3 += (double)x0.w;
-                        a0 += (double)x1.x; a1 += (double)x1.y;
-                        a2 += (double)x1.z; a3 += (double)x1.w;
+                for (int t0 = 0; t0 < nb; t0 += R * SK_U) {
+                    float4 x[SK_U];
+#pragma unroll
+                    for (int u = 0; u < SK_U; u++) {
+                        const int t = t0 + u * R + slot;
+                        const int64_t g = __shfl_sync(0xffffffffu, gl, min(t, 31));
+                        x[u] = (on && t < nb) ? __ldg(S4 + g * k4 + cc + c4) : z4;
                     }
-                }
-                for (; t < nb; t += R) {
-                    const int tb = t + slot;
-                    const int64_t g0 = __shfl_sync(0xffffffffu, gl, min(31, tb));
-                    if (on && tb < nb) {
-                        const float4 x0 = __ldg(S4 + g0 * k4 + cc + c4);
-                        a0 += (double)x0.x; a1 += (double)x0.y;
-                        a2 += (double)x0.z; a3 += (double)x0.w;
-                    }
+#pragma unroll
+                    for (int u = 0; u < SK_U; u++) add4(a0, a1, a2, a3, x[u]);
                 }
             }
             for (int sl = 1; sl < R; sl++) {
