@@ -48,6 +48,9 @@ enum { RFXC_UPPER_I32 = 0,  /* packed i<j rows [row_lo,row_hi), int32 counts    
        RFXC_UPPER_F64 = 1,  /* packed i<j rows, count/B in f64 (FullTriangle)    */
        RFXC_BLOCK_I32 = 2   /* (row_hi-row_lo, n) int32, j>i counted, else 0     */ };
 
+/* Bit 31 of a bucketed perm entry marks the first member of its leaf. */
+#define RFXC_PERM_FIRST 0x80000000u
+
 /* Quantisation modes (quantize.py:16). */
 enum { RFXC_Q_F32 = 0, RFXC_Q_F16 = 1, RFXC_Q_I8 = 2, RFXC_Q_NF4 = 3 };
 
@@ -120,13 +123,15 @@ int rfxc_transpose_i32(const int32_t* d_in, int64_t rows, int64_t cols,
  * accumulate_pair_counts[_block], _kernels.py:458-468, :491-501), done once
  * and reused by K3/K4.  Inputs: codes_tm (Bl x n), leaf_base (Bl+1, int64,
  * exclusive prefix of leaf_counts).  Outputs: d_perm (Bl x n): samples of
- * tree b sorted by leaf, ascending within a leaf; d_seg (leaf_base[Bl]+1):
- * absolute start of every leaf's run in d_perm (d_seg[last] = Bl*n).
- * d_scratch: 4 * leaf_base[Bl] bytes. */
+ * tree b sorted by leaf, ascending within a leaf, the first member of every
+ * leaf tagged with RFXC_PERM_FIRST; d_seg (leaf_base[Bl]+1): absolute start
+ * of every leaf's run in d_perm (d_seg[last] = Bl*n); *d_has_empty = 1 when
+ * some leaf has no member.  d_scratch: 4 * leaf_base[Bl] bytes (used only
+ * for trees with too many leaves for shared memory). */
 int rfxc_bucket(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
                 const int64_t* d_leaf_base, int32_t max_leaf_count,
-                int32_t* d_perm, int64_t* d_seg, int32_t* d_scratch,
-                void* stream);
+                uint32_t* d_perm, int64_t* d_seg, int32_t* d_scratch,
+                int32_t* d_has_empty, void* stream);
 
 /* -------------------------------------------------------------------- K3 */
 /* Exact same-leaf co-occurrence counts for rows [row_lo, row_hi), j > i,
@@ -172,7 +177,7 @@ int rfxc_pack_f32(const double* d_in, int64_t n, int32_t k, int32_t ld,
 /* Leaf sums S[g, :] = sum_{i in leaf g} X[i, :] for global leaves
  * [g_lo, g_hi) (one phase of Mt @ X, proximity.py:394).  X: f32 (n, ld);
  * S: f32 ((g_hi - g_lo), ld). */
-int rfxc_leaf_sums(const int32_t* d_perm, const int64_t* d_seg, int64_t g_lo,
+int rfxc_leaf_sums(const uint32_t* d_perm, const int64_t* d_seg, int64_t g_lo,
                    int64_t g_hi, const float* d_X, int32_t k, int32_t ld,
                    float* d_S, void* stream);
 
@@ -183,6 +188,26 @@ int rfxc_leaf_gather(const int32_t* d_codes_nb, int64_t n, int32_t Bl,
                      const int64_t* d_leaf_base, const float* d_S, int32_t k,
                      int32_t ld, double scale, int32_t accumulate, double* d_Y,
                      void* stream);
+
+/* One whole sketch pass Y = scale * sum_b E_b E_b^T X over the Bl local
+ * trees (M @ (Mt @ X) of proximity.py:394, :397, :398 with M the
+ * 1/sqrt(B)-scaled one-hot, so scale = 1/B) as one cooperative kernel:
+ * trees in batches of T whose leaf sums stay in L2 (leaf sums of batch e and
+ * gather of batch e-1 per grid-synchronised epoch).  X: f32 (n, ld), ld = k
+ * rounded up to 4 (k <= 128); Y: f64 (n, k).  rfxc_sketch_plan (host) picks
+ * T so that two batches of leaf sums fit budget_bytes and sizes the
+ * workspace; rfxc_sketch_prepare runs once per (bucketed membership, plan);
+ * d_perm / d_seg / d_has_empty come from rfxc_bucket.  Deterministic. */
+int rfxc_sketch_plan(const int32_t* h_leaf_counts, int32_t Bl, int64_t n, int32_t k,
+                     int64_t budget_bytes, int32_t* T_out, int64_t* s_rows_out,
+                     int64_t* work_bytes_out);
+int rfxc_sketch_prepare(const int64_t* d_seg, const int64_t* d_leaf_base, int64_t n,
+                        int32_t Bl, int32_t k, int32_t T, int64_t s_rows, void* d_work,
+                        void* stream);
+int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg, const int32_t* d_codes_nb,
+                     const int64_t* d_leaf_base, const int32_t* d_has_empty, int64_t n,
+                     int32_t Bl, const float* d_X, int32_t k, int32_t ld, double scale,
+                     int32_t T, int64_t s_rows, double* d_Y, void* d_work, void* stream);
 
 /* -------------------------------------------------------------------- K5 */
 /* C = A^T B for row-major f64 A (n, ka), B (n, kb): deterministic two-level

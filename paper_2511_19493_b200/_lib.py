@@ -41,7 +41,7 @@ SIGNATURES = {
     "rfxc_values_to_f32_host": (ctypes.c_int, [P, I64, P, P, I32]),
     "rfxc_leaf_codes": (ctypes.c_int, [P, P, I32, I32, I32, I32, P, I64, P, P]),
     "rfxc_transpose_i32": (ctypes.c_int, [P, I64, I64, P, P]),
-    "rfxc_bucket": (ctypes.c_int, [P, I64, I32, P, I32, P, P, P, P]),
+    "rfxc_bucket": (ctypes.c_int, [P, I64, I32, P, I32, P, P, P, P, P]),
     "rfxc_pair_counts": (ctypes.c_int, [P, I64, I32, I64, I64, I32, P, P]),
     "rfxc_triblock_count": (ctypes.c_int, [P, I64, I32, I64, I64, F64, P, P]),
     "rfxc_triblock_emit": (ctypes.c_int, [P, I64, I32, I64, I64, F64, P, P, P, P, P, P, P,
@@ -51,6 +51,10 @@ SIGNATURES = {
     "rfxc_pack_f32": (ctypes.c_int, [P, I64, I32, I32, P, P]),
     "rfxc_leaf_sums": (ctypes.c_int, [P, P, I64, I64, P, I32, I32, P, P]),
     "rfxc_leaf_gather": (ctypes.c_int, [P, I64, I32, P, P, I32, I32, F64, I32, P, P]),
+    "rfxc_sketch_plan": (ctypes.c_int, [P, I32, I64, I32, I64, P, P, P]),
+    "rfxc_sketch_prepare": (ctypes.c_int, [P, P, I64, I32, I32, I32, I64, P, P]),
+    "rfxc_sketch_pass": (ctypes.c_int, [P, P, P, P, P, I64, I32, P, I32, I32, F64, I32, I64, P, P,
+                                        P]),
     "rfxc_gram_parts": (ctypes.c_int, [I64]),
     "rfxc_gram": (ctypes.c_int, [P, P, I64, I32, I32, P, P, P]),
     "rfxc_matmul_small": (ctypes.c_int, [P, I64, I32, P, I32, P, P, I32, P]),
@@ -104,6 +108,7 @@ LAUNCHES = {"rfxc_values_to_f32": 1, "rfxc_forest_pack": 1, "rfxc_leaf_codes": 1
             "rfxc_transpose_i32": 1, "rfxc_bucket": 1, "rfxc_pair_counts": 1,
             "rfxc_triblock_count": 1, "rfxc_triblock_emit": 1, "rfxc_exclusive_scan_i64": 1,
             "rfxc_normals": 1, "rfxc_pack_f32": 1, "rfxc_leaf_sums": 1, "rfxc_leaf_gather": 1,
+            "rfxc_sketch_prepare": 1, "rfxc_sketch_pass": 1,
             "rfxc_gram": 2, "rfxc_matmul_small": 1, "rfxc_factor_quantize": 3,
             "rfxc_dequantize": 1, "rfxc_pmax": 2, "rfxc_mds_power": 1, "rfxc_gram_matvec": 1}
 launch_count = 0

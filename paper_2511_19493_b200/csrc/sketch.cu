@@ -18,7 +18,14 @@
 // Both are deterministic (no atomics), so the factors are bit-reproducible
 // run to run, as the reference's are (tests/test_proximity.py:229-232).
 #include "../csrc/host/pcg32.h"
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+#include <vector>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rfxc {
 
@@ -101,7 +108,7 @@ leaf_sums_kernel(const int32_t* __restrict__ perm, const int64_t* __restrict__ s
                 double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
                 for (int64_t base = s; base < e; base += 32) {
                     const int m = (int)min64(32, e - base);
-                    const int32_t rid = lane < m ? __ldg(perm + base + lane) : 0;
+                    const int32_t rid = lane < m ? (__ldg(perm + base + lane) & 0x7fffffff) : 0;
                     for (int t0 = 0; t0 < m; t0 += R * SK_U) {
                         float4 x[SK_U];
 #pragma unroll
@@ -304,6 +311,450 @@ matmul_small_kernel(const double* __restrict__ Y, int64_t n, int ka, const doubl
     }
 }
 
+
+// ============================================================ fused pass
+// One sketch pass Y = scale * sum_b E_b E_b^T X as a single cooperative
+// kernel.  Trees are processed in batches of T (sized so that the leaf sums
+// of two batches, X and Y stay in L2); epoch e computes the leaf sums of
+// batch e (phase A) and gathers batch e-1 into Y (phase B), then a grid
+// barrier.  Leaf sums therefore never leave L2, where the two-kernel path
+// writes all sum(L) x ld sums to HBM and gathers them back per (sample, tree).
+//
+// Phase A (warp item = 256 consecutive positions of the bucketed perm):
+// the 32 member rows of a sub-chunk are copied into shared memory with
+// cp.async (one row per lane, next sub-chunk in flight while this one is
+// reduced), then lanes own column pairs and walk the positions in order,
+// closing a leaf at every RFXC_PERM_FIRST flag (f64 accumulation, fixed
+// order).  Leaves cut by an item boundary leave one f64 piece per item;
+// the last piece to arrive (per-leaf counter) adds the pieces in item order
+// and writes the sum, so results are bit-reproducible.
+// Phase B (warp item = 16 samples): lane t reads the sample's code in tree
+// b0+t (one coalesced row segment of the (n, B) membership), then the T
+// leaf-sum rows are gathered as float4 lanes with f64 accumulation and
+// added to Y (scaled by 1/B in the last batch).
+constexpr int SKP_ITEM = 384;     // positions per phase-A item (12 sub-chunks of 32)
+constexpr int SKP_SAMPLES = 24;  // samples per phase-B item
+constexpr int SKP_RMAX = 4;      // row slots per warp (lane groups of k4 lanes)
+constexpr int SKP_MAX_T = 32;
+
+struct SkpLayout {
+    int64_t S, part, cnt, ctr, item_leaf, total;
+};
+
+__host__ __device__ inline int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
+
+__host__ __device__ inline int64_t skp_items_per_batch(int64_t n, int T)
+{
+    return (T * n + SKP_ITEM - 1) / SKP_ITEM;
+}
+
+__host__ __device__ inline int skp_nbatch(int Bl, int T) { return (Bl + T - 1) / T; }
+
+__host__ __device__ inline SkpLayout skp_layout(int64_t n, int Bl, int T, int ld, int k,
+                                                int64_t s_rows)
+{
+    SkpLayout L;
+    const int64_t ipb = skp_items_per_batch(n, T);
+    const int nb = skp_nbatch(Bl, T);
+    int64_t off = 0;
+    L.S = off;         off += align256(2 * s_rows * ld * 4);
+    L.part = off;      off += align256(2 * ipb * ld * 8);
+    L.cnt = off;       off += align256(s_rows * 4);
+    L.ctr = off;       off += align256(2 * (int64_t)(nb + 1) * 4);
+    L.item_leaf = off; off += align256(nb * ipb * 4);
+    L.total = off;
+    return L;
+}
+
+struct SkpArgs {
+    const uint32_t* perm;
+    const int64_t* seg;
+    const int32_t* codes;      // (n, Bl)
+    const int64_t* leaf_base;  // (Bl + 1)
+    const int32_t* has_empty;
+    const float* X;            // (n, ld)
+    double* Y;                 // (n, k)
+    float* S;                  // 2 x s_rows x ld
+    double* part;              // ipb x 2 x k
+    int32_t* cnt;              // s_rows
+    unsigned* ctr;             // 2 x (nbatch + 1)
+    const int32_t* item_leaf;  // nbatch x ipb
+    int64_t n, s_rows, ipb;
+    int Bl, k, ld, T, nbatch;
+    double scale;
+    unsigned long long* timing;  // debug (RFXC_SKETCH_TIMING): per warp, per epoch work ns
+};
+
+// item_leaf[e * ipb + it]: global leaf containing the first position of item
+// it of batch e (last g with seg[g] <= P < seg[g + 1]).
+__global__ void skp_item_leaf_kernel(const int64_t* __restrict__ seg,
+                                     const int64_t* __restrict__ leaf_base, int64_t n, int Bl,
+                                     int T, int64_t ipb, int32_t* __restrict__ item_leaf)
+{
+    const int nb = skp_nbatch(Bl, T);
+    const int64_t total = nb * ipb;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(q / ipb);
+        const int64_t it = q % ipb;
+        const int b0 = e * T, b1 = min(Bl, b0 + T);
+        const int64_t P = (int64_t)b0 * n + it * SKP_ITEM;
+        if (P >= (int64_t)b1 * n) {
+            item_leaf[q] = -1;
+            continue;
+        }
+        int64_t a = leaf_base[b0], z = leaf_base[b1];  // answer in [a, z)
+        while (z - a > 1) {
+            const int64_t m = (a + z) >> 1;
+            if (seg[m] <= P) a = m;
+            else z = m;
+        }
+        item_leaf[q] = (int32_t)a;
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Emit one finished (or cut) leaf segment held by the slot-0 lanes (lane c4
+// owns columns 4c4..4c4+3 in f64).  kind: 0 = whole leaf, 1 = first segment
+// of the item cut at its start, 2 = last segment cut at its end, 3 = both
+// (the item lies inside the leaf).  Cut segments leave an f64 piece per item;
+// the last piece to arrive adds them in item order and writes the sum.
+__device__ __forceinline__ void skp_emit(const SkpArgs& A, const double* acc, int64_t g, int kind, int64_t it,
+                         int64_t pos0, int64_t g0, float4* Sb, int lane, bool lead)
+{
+    const int k4 = A.ld >> 2;
+    if (kind == 0) {
+        if (lead) Sb[(g - g0) * k4 + lane] = make_float4((float)acc[0], (float)acc[1],
+                                                         (float)acc[2], (float)acc[3]);
+        return;
+    }
+    const int slot = kind == 2 ? 1 : 0;
+    double* pp = A.part + (it * 2 + slot) * A.ld + 4 * lane;
+    if (lead) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) pp[q] = acc[q];
+    }
+    __threadfence();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+        const int64_t s = A.seg[g], e = A.seg[g + 1];
+        const int npieces = (int)(((e - 1 - pos0) / SKP_ITEM) - ((s - pos0) / SKP_ITEM)) + 1;
+        const int old = atomicAdd(A.cnt + (g - g0), 1);
+        last = (old == npieces - 1);
+        if (last) A.cnt[g - g0] = 0;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();
+    if (lead) {
+        const int64_t s = A.seg[g], e = A.seg[g + 1];
+        const int64_t i0 = (s - pos0) / SKP_ITEM, i1 = (e - 1 - pos0) / SKP_ITEM;
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int64_t j = i0; j <= i1; j++) {
+            const double* src = A.part + (j * 2 + (j == i0 ? 1 : 0)) * A.ld + 4 * lane;
+#pragma unroll
+            for (int q = 0; q < 4; q++) t[q] += __ldcg(src + q);
+        }
+        Sb[(g - g0) * k4 + lane] = make_float4((float)t[0], (float)t[1], (float)t[2], (float)t[3]);
+    }
+}
+
+__device__ __forceinline__ void f4add(float4& a, const float4 x)
+{
+    a.x += x.x;
+    a.y += x.y;
+    a.z += x.z;
+    a.w += x.w;
+}
+
+// slot partials (lane = slot * k4 + c4) -> slot 0, fixed order
+__device__ __forceinline__ void slot_combine(float4& a, int R, int k4, int slot, int lane)
+{
+    for (int sl = 1; sl < R; sl++) {
+        const int src = min(31, lane + sl * k4);
+        const float ox = __shfl_sync(0xffffffffu, a.x, src);
+        const float oy = __shfl_sync(0xffffffffu, a.y, src);
+        const float oz = __shfl_sync(0xffffffffu, a.z, src);
+        const float ow = __shfl_sync(0xffffffffu, a.w, src);
+        if (slot == 0) {
+            a.x += ox;
+            a.y += oy;
+            a.z += oz;
+            a.w += ow;
+        }
+    }
+}
+
+// Per-warp shared scratch: SKP_RMAX x 32 uint32 (phase A perm values /
+// phase B leaf-sum row ids).
+constexpr int SKP_SCRATCH = SKP_RMAX * 32;
+constexpr int SKP_U = 8;  // row loads in flight per lane
+
+// Phase A item: positions [P0, P1) of batch e, in steps of R sub-chunks of
+// 32 positions.  Slot s (lanes s*k4 .. s*k4+k4-1, lane c4 owning float4
+// column c4) walks sub-chunk s of the step in position order with coalesced
+// row loads (SKP_U in flight), summing each leaf segment in f32 and writing
+// the leaf sums of segments that start and end inside its sub-chunk.  The
+// segments cut by sub-chunk boundaries (head / tail partials of every slot)
+// are then joined in position order into one f64 carry held by every slot,
+// which is emitted when its leaf ends (a piece when cut by the item edge).
+// Leaf ids follow from the first-member flags (no empty leaves on this path).
+__device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf, int lane)
+{
+    const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
+    const int64_t pos0 = (int64_t)b0 * A.n, pend = (int64_t)b1 * A.n;
+    const int64_t P0 = pos0 + it * SKP_ITEM, P1 = min64(P0 + SKP_ITEM, pend);
+    const int64_t g0 = A.leaf_base[b0];
+    float4* Sb = reinterpret_cast<float4*>(A.S + (int64_t)(e & 1) * A.s_rows * A.ld);
+    const int k4 = A.ld >> 2;
+    const int R = min(SKP_RMAX, 32 / k4);
+    const int slot = lane / k4, c4 = lane - slot * k4;
+    const bool on = slot < R;
+    const int nsub = (int)((P1 - P0 + 31) >> 5);
+    const float4* X4 = reinterpret_cast<const float4*>(A.X);
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+
+    int tail_first = 1;
+    if (lane == 0 && P1 < pend) tail_first = (__ldg(A.perm + P1) & RFXC_PERM_FIRST) != 0;
+    const bool tail_open = !__shfl_sync(0xffffffffu, tail_first, 0);
+    const int64_t gi = A.item_leaf[(int64_t)e * A.ipb + it];
+
+    // carry: the open segment at the current position (f64, every lane holds
+    // its column group), its leaf, whether it was cut at the item start and
+    // whether it holds any row yet
+    double cy[4] = {0.0, 0.0, 0.0, 0.0};
+    int64_t cleaf = gi;
+    int ckind = 1;
+    bool cvalid = false;
+    int64_t flags_before = 0;  // flagged positions in (P0, current sub-chunk start)
+
+    uint32_t pv[SKP_RMAX];
+    auto load_pv = [&](int s0) {
+#pragma unroll
+        for (int j = 0; j < SKP_RMAX; j++) {
+            const int64_t q = P0 + 32 * (int64_t)(s0 + j) + lane;
+            pv[j] = (j < R && s0 + j < nsub && q < P1) ? __ldg(A.perm + q) : 0u;
+        }
+    };
+    load_pv(0);
+    for (int s0 = 0; s0 < nsub; s0 += R) {
+        unsigned fl[SKP_RMAX];
+        int mm[SKP_RMAX];
+#pragma unroll
+        for (int j = 0; j < SKP_RMAX; j++) {
+            mm[j] = (int)max64(0, min64(32, P1 - (P0 + 32 * (int64_t)(s0 + j))));
+            fl[j] = __ballot_sync(0xffffffffu, lane < mm[j] && (pv[j] & RFXC_PERM_FIRST));
+            pbuf[j * 32 + lane] = pv[j] & ~RFXC_PERM_FIRST;
+        }
+        if (s0 == 0 && (fl[0] & 1u)) { ckind = 0; }  // the item starts a leaf
+        __syncwarp();
+        if (s0 + R < nsub) load_pv(s0 + R);  // prefetch the next step's perm values
+        // this slot's sub-chunk
+        unsigned fs = 0;
+        int m = 0;
+        int64_t before = flags_before;
+#pragma unroll
+        for (int j = 0; j < SKP_RMAX; j++) {
+            const unsigned fj = (s0 == 0 && j == 0) ? (fl[j] & ~1u) : fl[j];  // P0 itself never counts
+            if (j == slot) { fs = fl[j]; m = mm[j]; }
+            if (j < slot) before += __popc(fj);
+        }
+        const bool first_sub = (s0 == 0 && slot == 0);
+        int64_t cur = gi + before + ((fs & 1u) && !first_sub ? 1 : 0);
+        bool inside = (fs & 1u) != 0;  // current segment started inside this sub-chunk
+        float4 acc = z4, head = z4;
+        const uint32_t* pb = pbuf + slot * 32;
+        for (int p0 = 0; p0 < 32; p0 += SKP_U) {
+            float4 x[SKP_U];
+#pragma unroll
+            for (int u = 0; u < SKP_U; u++) {
+                const int p = p0 + u;
+                x[u] = (on && p < m) ? __ldg(X4 + (int64_t)pb[p] * k4 + c4) : z4;
+            }
+#pragma unroll
+            for (int u = 0; u < SKP_U; u++) {
+                const int p = p0 + u;
+                if (p > 0 && p < m && ((fs >> p) & 1u)) {  // a leaf starts at p
+                    if (inside) {
+                        if (on) Sb[(cur - g0) * k4 + c4] = acc;
+                    } else {
+                        head = acc;
+                    }
+                    cur++;
+                    inside = true;
+                    acc = z4;
+                }
+                f4add(acc, x[u]);
+            }
+        }
+        // join the slots' cut segments in position order (uniform over the warp)
+#pragma unroll
+        for (int j = 0; j < SKP_RMAX; j++) {
+            if (j >= R || s0 + j >= nsub) break;
+            const int src = j * k4 + c4;
+            const float4 hj = make_float4(__shfl_sync(0xffffffffu, head.x, src),
+                                          __shfl_sync(0xffffffffu, head.y, src),
+                                          __shfl_sync(0xffffffffu, head.z, src),
+                                          __shfl_sync(0xffffffffu, head.w, src));
+            const float4 tj = make_float4(__shfl_sync(0xffffffffu, acc.x, src),
+                                          __shfl_sync(0xffffffffu, acc.y, src),
+                                          __shfl_sync(0xffffffffu, acc.z, src),
+                                          __shfl_sync(0xffffffffu, acc.w, src));
+            const int64_t curj = __shfl_sync(0xffffffffu, cur, j * k4);
+            const unsigned fj = (s0 == 0 && j == 0) ? (fl[j] & ~1u) : fl[j];
+            const bool starts = (fl[j] & 1u) != 0;
+            if (fj == 0 && !starts) {  // the whole sub-chunk continues the carry
+                cy[0] += (double)tj.x;
+                cy[1] += (double)tj.y;
+                cy[2] += (double)tj.z;
+                cy[3] += (double)tj.w;
+                cvalid = true;
+                continue;
+            }
+            if (!starts) {  // head rows close the carried leaf
+                cy[0] += (double)hj.x;
+                cy[1] += (double)hj.y;
+                cy[2] += (double)hj.z;
+                cy[3] += (double)hj.w;
+                cvalid = true;
+            }
+            if (cvalid && (fj != 0)) skp_emit(A, cy, cleaf, ckind, it, pos0, g0, Sb, lane, slot == 0);
+            // the last segment of sub-chunk j becomes the carry
+            cy[0] = (double)tj.x;
+            cy[1] = (double)tj.y;
+            cy[2] = (double)tj.z;
+            cy[3] = (double)tj.w;
+            cleaf = curj;
+            if (fj != 0) ckind = 0;
+            cvalid = true;
+        }
+#pragma unroll
+        for (int j = 0; j < SKP_RMAX; j++) {
+            if (j >= R || s0 + j >= nsub) break;
+            flags_before += __popc((s0 == 0 && j == 0) ? (fl[j] & ~1u) : fl[j]);
+        }
+        __syncwarp();
+    }
+    const int kind = tail_open ? (ckind ? 3 : 2) : ckind;
+    skp_emit(A, cy, cleaf, kind, it, pos0, g0, Sb, lane, slot == 0);
+}
+
+// Phase B item: samples [i0, i0 + SKP_SAMPLES) against batch e's leaf sums.
+// Slot s takes every R-th sample; its lanes gather the nT leaf-sum rows of
+// that sample (coalesced, SKP_U in flight), sum them in f32 and add the sum
+// to Y in f64 (scaled by 1/B in the last batch).
+__device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf, int lane)
+{
+    const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
+    const int nT = b1 - b0;
+    const int64_t g0 = A.leaf_base[b0];
+    const float4* Sb = reinterpret_cast<const float4*>(A.S + (int64_t)(e & 1) * A.s_rows * A.ld);
+    const int k4 = A.ld >> 2;
+    const int R = min(SKP_RMAX, 32 / k4);
+    const int slot = lane / k4, c4 = lane - slot * k4;
+    const bool on = slot < R;
+    const bool first = e == 0, last = e == A.nbatch - 1;
+    const int64_t i0 = it * SKP_SAMPLES, i1 = min64(i0 + SKP_SAMPLES, A.n);
+    const int32_t lb = lane < nT ? (int32_t)(A.leaf_base[b0 + lane] - g0) : 0;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int* rb = reinterpret_cast<const int*>(rbuf) + slot * 32;
+
+    int32_t cn[SKP_RMAX];
+    auto load_codes = [&](int64_t ib) {
+#pragma unroll
+        for (int j = 0; j < SKP_RMAX; j++) {
+            const int64_t i = ib + j;
+            cn[j] = (j < R && i < i1 && lane < nT) ? __ldg(A.codes + i * A.Bl + b0 + lane) : 0;
+        }
+    };
+    load_codes(i0);
+    for (int64_t ib = i0; ib < i1; ib += R) {
+#pragma unroll
+        for (int j = 0; j < SKP_RMAX; j++) reinterpret_cast<int*>(rbuf)[j * 32 + lane] = lb + cn[j];
+        __syncwarp();
+        if (ib + R < i1) load_codes(ib + R);
+        const int64_t i = ib + slot;
+        const bool act = on && i < i1;
+        double yo[4] = {0.0, 0.0, 0.0, 0.0};
+        double* y = A.Y + i * A.k + 4 * c4;
+        if (act && !first) {
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (4 * c4 + q < A.k) yo[q] = y[q];
+        }
+        float4 acc = z4;
+        for (int t0 = 0; t0 < nT; t0 += SKP_U) {
+            float4 x[SKP_U];
+#pragma unroll
+            for (int u = 0; u < SKP_U; u++) {
+                const int t = t0 + u;
+                x[u] = (act && t < nT) ? __ldg(Sb + (int64_t)rb[t] * k4 + c4) : z4;
+            }
+#pragma unroll
+            for (int u = 0; u < SKP_U; u++) f4add(acc, x[u]);
+        }
+        if (act) {
+            const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                if (4 * c4 + q < A.k) {
+                    const double v = yo[q] + (double)a4[q];
+                    y[q] = last ? v * A.scale : v;
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) sketch_pass_kernel(SkpArgs A)
+{
+    extern __shared__ __align__(16) uint32_t skp_smem[];
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wpc = blockDim.x >> 5;
+    uint32_t* scratch = skp_smem + warp * SKP_SCRATCH;
+    const int64_t wg = (int64_t)blockIdx.x * wpc + warp;
+    const int64_t nB = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
+    for (int e = 0; e <= A.nbatch; e++) {
+        int64_t nA = 0;
+        if (e < A.nbatch) {
+            const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
+            nA = ((int64_t)(b1 - b0) * A.n + SKP_ITEM - 1) / SKP_ITEM;
+        }
+        const int64_t nb = e >= 1 ? nB : 0;
+        unsigned long long t0 = 0;
+        if (A.timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        // dynamic: A items first (longer), then B items; the next index is
+        // fetched while the current item runs
+        unsigned* ctr = A.ctr + 2 * e;
+        unsigned q = 0, qn = 0;
+        if (lane == 0) q = atomicAdd(ctr, 1u);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        while (q < nA + nb) {
+            if (lane == 0) qn = atomicAdd(ctr, 1u);
+            if (q < nA) skp_phase_a(A, e, q, scratch, lane);
+            else skp_phase_b(A, e - 1, q - nA, scratch, lane);
+            q = __shfl_sync(0xffffffffu, qn, 0);
+        }
+        if (A.timing && lane == 0) {
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            A.timing[(int64_t)e * 148 * 64 + wg] = t1 - t0;
+        }
+        grid.sync();
+    }
+}
+
 }  // namespace rfxc
 
 using namespace rfxc;
@@ -329,7 +780,7 @@ extern "C" int rfxc_pack_f32(const double* d_in, int64_t n, int32_t k, int32_t l
     return check_launch("pack_f32");
 }
 
-extern "C" int rfxc_leaf_sums(const int32_t* d_perm, const int64_t* d_seg, int64_t g_lo,
+extern "C" int rfxc_leaf_sums(const uint32_t* d_perm, const int64_t* d_seg, int64_t g_lo,
                               int64_t g_hi, const float* d_X, int32_t k, int32_t ld, float* d_S,
                               void* stream)
 {
@@ -339,7 +790,8 @@ extern "C" int rfxc_leaf_sums(const int32_t* d_perm, const int64_t* d_seg, int64
     const int64_t warps = g_hi - g_lo;
     int grid = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)sm_count() * 32);
     leaf_sums_kernel<<<grid, 256, 0, as_stream(stream)>>>(
-        d_perm, d_seg, g_lo, g_hi, reinterpret_cast<const float4*>(d_X), ld / 4,
+        reinterpret_cast<const int32_t*>(d_perm), d_seg, g_lo, g_hi,
+        reinterpret_cast<const float4*>(d_X), ld / 4,
         reinterpret_cast<float4*>(d_S));
     return check_launch("leaf_sums");
 }
@@ -398,4 +850,139 @@ extern "C" int rfxc_matmul_small(const double* d_Y, int64_t n, int32_t ka, const
     matmul_small_kernel<<<(unsigned)ceil_div(n, 16), 256, smem, as_stream(stream)>>>(
         d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32);
     return check_launch("matmul_small");
+}
+
+extern "C" int rfxc_sketch_plan(const int32_t* h_leaf_counts, int32_t Bl, int64_t n, int32_t k,
+                                int64_t budget_bytes, int32_t* T_out, int64_t* s_rows_out,
+                                int64_t* work_bytes_out)
+{
+    if (Bl < 1 || n < 1 || k < 1) return fail(RFXC_EDATA, "sketch_plan: bad shape");
+    const int ld = (k + 3) / 4 * 4;
+    int T = std::min(SKP_MAX_T, (int)Bl);
+    int64_t s_rows = 0;
+    for (; T >= 1; T--) {
+        s_rows = 0;
+        for (int b0 = 0; b0 < Bl; b0 += T) {
+            int64_t s = 0;
+            for (int b = b0; b < std::min<int>(Bl, b0 + T); b++) s += h_leaf_counts[b];
+            s_rows = std::max(s_rows, s);
+        }
+        if (2 * s_rows * ld * 4 <= budget_bytes || T == 1) break;
+    }
+    if (T_out) *T_out = T;
+    if (s_rows_out) *s_rows_out = std::max<int64_t>(s_rows, 1);
+    if (work_bytes_out) *work_bytes_out = skp_layout(n, Bl, T, ld, k, std::max<int64_t>(s_rows, 1)).total;
+    return RFXC_OK;
+}
+
+extern "C" int rfxc_sketch_prepare(const int64_t* d_seg, const int64_t* d_leaf_base, int64_t n,
+                                   int32_t Bl, int32_t k, int32_t T, int64_t s_rows, void* d_work,
+                                   void* stream)
+{
+    if (n < 1 || Bl < 1 || k < 1 || T < 1 || T > SKP_MAX_T || s_rows < 1)
+        return fail(RFXC_EDATA, "sketch_prepare: bad shape");
+    const int ld = (k + 3) / 4 * 4;
+    const SkpLayout L = skp_layout(n, Bl, T, ld, k, s_rows);
+    char* w = static_cast<char*>(d_work);
+    cudaStream_t st = as_stream(stream);
+    cudaError_t e = cudaMemsetAsync(w + L.cnt, 0, s_rows * 4, st);
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "sketch_prepare: %s", cudaGetErrorString(e));
+    const int64_t ipb = skp_items_per_batch(n, T);
+    const int64_t total = skp_nbatch(Bl, T) * ipb;
+    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 8);
+    skp_item_leaf_kernel<<<grid, 256, 0, st>>>(d_seg, d_leaf_base, n, Bl, T, ipb,
+                                               reinterpret_cast<int32_t*>(w + L.item_leaf));
+    return check_launch("sketch_prepare");
+}
+
+static int launch_skp(SkpArgs& A, cudaStream_t st)
+{
+    auto kern = sketch_pass_kernel;
+    const int warps = 8;
+    const size_t smem = (size_t)warps * SKP_SCRATCH * 4;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "sketch_pass attr: %s", cudaGetErrorString(e));
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * warps, smem);
+    if (occ < 1) return fail(RFXC_ERUNTIME, "sketch_pass: kernel does not fit an SM (ld=%d)", A.ld);
+    void* args[] = {&A};
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(sm_count() * occ), dim3(32 * warps),
+                                    args, smem, st);
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "sketch_pass launch: %s", cudaGetErrorString(e));
+    return check_launch("sketch_pass");
+}
+
+extern "C" int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg,
+                                const int32_t* d_codes_nb, const int64_t* d_leaf_base,
+                                const int32_t* d_has_empty, int64_t n, int32_t Bl,
+                                const float* d_X, int32_t k, int32_t ld, double scale, int32_t T,
+                                int64_t s_rows, double* d_Y, void* d_work, void* stream)
+{
+    if (n < 1 || Bl < 1 || k < 1 || ld != (k + 3) / 4 * 4 || T < 1 || T > SKP_MAX_T || s_rows < 1)
+        return fail(RFXC_EDATA, "sketch_pass: bad shape (ld must be k rounded up to 4)");
+    if (ld > 128) return fail(RFXC_EDATA, "sketch_pass: k=%d above 128", k);
+    const SkpLayout L = skp_layout(n, Bl, T, ld, k, s_rows);
+    char* w = static_cast<char*>(d_work);
+    cudaStream_t st = as_stream(stream);
+    SkpArgs A;
+    A.perm = d_perm;
+    A.seg = d_seg;
+    A.codes = d_codes_nb;
+    A.leaf_base = d_leaf_base;
+    A.has_empty = d_has_empty;
+    A.X = d_X;
+    A.Y = d_Y;
+    A.S = reinterpret_cast<float*>(w + L.S);
+    A.part = reinterpret_cast<double*>(w + L.part);
+    A.cnt = reinterpret_cast<int32_t*>(w + L.cnt);
+    A.ctr = reinterpret_cast<unsigned*>(w + L.ctr);
+    A.item_leaf = reinterpret_cast<const int32_t*>(w + L.item_leaf);
+    A.n = n;
+    A.s_rows = s_rows;
+    A.ipb = skp_items_per_batch(n, T);
+    A.Bl = Bl;
+    A.k = k;
+    A.ld = ld;
+    A.T = T;
+    A.nbatch = skp_nbatch(Bl, T);
+    A.scale = scale;
+    cudaError_t e = cudaMemsetAsync(A.ctr, 0, 2 * (size_t)(A.nbatch + 1) * 4, st);
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "sketch_pass: %s", cudaGetErrorString(e));
+    A.timing = nullptr;
+    if (!getenv("RFXC_SKETCH_TIMING")) return launch_skp(A, st);
+    // debug: per-warp work time per epoch, summarised on stderr (synchronous)
+    const int64_t nWk = (int64_t)sm_count() * 64;  // >= warps of any launch
+    const size_t slots = (size_t)(A.nbatch + 1) * nWk;
+    cudaMalloc(&A.timing, slots * 8);
+    cudaMemsetAsync(A.timing, 0, slots * 8, st);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    int rc = launch_skp(A, st);
+    cudaEventRecord(e1, st);
+    cudaStreamSynchronize(st);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    std::vector<unsigned long long> h(slots);
+    cudaMemcpy(h.data(), A.timing, slots * 8, cudaMemcpyDeviceToHost);
+    cudaFree(A.timing);
+    const int64_t nW = nWk;
+    double sum_max = 0;
+    for (int ep = 0; ep <= A.nbatch; ep++) {
+        unsigned long long mx = 0, tot = 0;
+        int64_t cnt = 0;
+        for (int64_t w = 0; w < nW; w++) {
+            const unsigned long long v = h[(size_t)ep * nW + w];
+            if (v) { mx = std::max(mx, v); tot += v; cnt++; }
+        }
+        sum_max += mx * 1e-6;
+        if (ep < 3 || ep == A.nbatch)
+            fprintf(stderr, "[sketch] epoch %d: warps %lld mean %.1f us max %.1f us\n", ep,
+                    (long long)cnt, cnt ? tot / 1e3 / cnt : 0.0, mx / 1e3);
+    }
+    fprintf(stderr, "[sketch] pass %.3f ms, sum of per-epoch max work %.3f ms, T=%d epochs=%d\n",
+            ms, sum_max, A.T, A.nbatch + 1);
+    return rc;
 }

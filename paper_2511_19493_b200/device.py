@@ -6,7 +6,8 @@ HBM layout (one process per GPU):
   nodes    packed node records of the local trees, 8 B (f32) / 16 B (f64)
   codes_tm (Bl, n) int32  — traversal output, bucketing input
   codes_nb (n, Bl) int32  — LeafMembership.codes layout, sketch/pairs input
-  perm     (Bl, n) int32  — samples sorted by leaf per tree (K2)
+  perm     (Bl, n) int32  — samples sorted by leaf per tree (K2), bit 31 set
+                            on the first member of every leaf
   seg      (sum L + 1) int64 — start of every leaf's run in perm
   leaf_base (Bl + 1) int64 — global leaf id of each tree's leaf 0
 Everything stays on the device between calls; host arrays are produced
@@ -180,6 +181,7 @@ class DeviceMembership:
         self.total_leaves = int(base[-1])
         self._perm = None
         self._seg = None
+        self._has_empty = None
 
     @property
     def Bl(self) -> int:
@@ -198,12 +200,19 @@ class DeviceMembership:
             seg = torch.empty(self.total_leaves + 1, dtype=torch.int64, device=dev)
             maxl = int(self.leaf_counts.max())
             scratch = torch.empty(max(self.total_leaves, 1), dtype=torch.int32, device=dev)
+            has_empty = torch.empty(1, dtype=torch.int32, device=dev)
             with region("bucket"):
                 _lib.call("rfxc_bucket", _lib.ptr(self.codes_tm), self.n, self.Bl,
                           _lib.ptr(self.leaf_base), maxl, _lib.ptr(perm), _lib.ptr(seg),
-                          _lib.ptr(scratch), _lib.stream_handle())
-            self._perm, self._seg = perm, seg
+                          _lib.ptr(scratch), _lib.ptr(has_empty), _lib.stream_handle())
+            self._perm, self._seg, self._has_empty = perm, seg, has_empty
         return self._perm, self._seg
+
+    @property
+    def has_empty(self):
+        """Device int32 flag: some local leaf has no member (from K2)."""
+        self.buckets()
+        return self._has_empty
 
     @classmethod
     def from_host(cls, codes: np.ndarray, leaf_counts: np.ndarray):

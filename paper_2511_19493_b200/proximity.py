@@ -19,6 +19,7 @@ sketch partials with torch.distributed (NCCL) — the only collective.
 from __future__ import annotations
 
 import logging
+import os
 from collections.abc import Mapping
 from dataclasses import dataclass, field
 
@@ -473,37 +474,91 @@ class LowRankQuantized:
         return self.factor.payload_nbytes()
 
 
-class _Sketch:
-    """P X for the (local trees of the) membership: leaf sums + gather, and
-    the all-reduce of the partials when the membership is a tree shard."""
+def _l2_bytes() -> int:
+    import ctypes
+    import torch
+    sm, l2, smem = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
+    _lib.call("rfxc_device_info", torch.cuda.current_device(), ctypes.byref(sm), ctypes.byref(l2),
+              ctypes.byref(smem))
+    return int(l2.value)
 
-    def __init__(self, d: DeviceMembership, k: int, group=None):
+
+# fraction of L2 the sketch may fill with X, Y and two batches of leaf sums
+SKETCH_L2_FRACTION = float(os.environ.get("RFX_SKETCH_L2_FRACTION", "0.75"))
+SKETCH_FUSED_MAX_LD = 128
+
+
+class _Sketch:
+    """P X for the (local trees of the) membership, and the all-reduce of the
+    partials when the membership is a tree shard.
+
+    k <= 128: one fused cooperative kernel per pass (rfxc_sketch_pass, leaf
+    sums batched so they stay L2-resident); wider sketches use the two-kernel
+    leaf_sums / leaf_gather path."""
+
+    def __init__(self, d: DeviceMembership, k: int, group=None, budget: int | None = None):
+        import ctypes
         import torch
         self.d = d
         self.k = k
         self.ld = (k + 3) // 4 * 4
         self.perm, self.seg = d.buckets()
         dev = d.codes_nb.device
-        self.S = torch.empty((max(d.total_leaves, 1), self.ld), dtype=torch.float32, device=dev)
         self.group = group
+        # the fused pass derives leaf ids from first-member flags, which needs
+        # every leaf non-empty (always true for a forest's own training set)
+        self.fused = self.ld <= SKETCH_FUSED_MAX_LD and not int(d.has_empty.item())
+        if self.fused:
+            if budget is None:  # two batches of leaf sums next to X and Y in L2
+                budget = int(SKETCH_L2_FRACTION * _l2_bytes()) - d.n * self.ld * 4 - d.n * k * 8
+                budget = max(budget, 8 << 20)
+            T, rows, wb = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+            lc = np.ascontiguousarray(d.leaf_counts, dtype=np.int32)
+            _lib.call("rfxc_sketch_plan", lc.ctypes.data_as(_lib.P), d.Bl, d.n, k, budget,
+                      ctypes.byref(T), ctypes.byref(rows), ctypes.byref(wb))
+            self.T, self.s_rows = int(T.value), int(rows.value)
+            self.work = torch.empty(int(wb.value), dtype=torch.uint8, device=dev)
+            _lib.call("rfxc_sketch_prepare", _lib.ptr(self.seg), _lib.ptr(d.leaf_base), d.n, d.Bl,
+                      k, self.T, self.s_rows, _lib.ptr(self.work), _lib.stream_handle())
+        else:
+            self.S = torch.empty((max(d.total_leaves, 1), self.ld), dtype=torch.float32,
+                                 device=dev)
 
     def apply(self, X32, kk: int, reduce: bool = True):
         """P X as (n, kk) f64; X32 is the (n, ld) f32 copy of X (zero beyond kk)."""
         import torch
         d = self.d
         Y = torch.empty((d.n, kk), dtype=torch.float64, device=X32.device)
-        with region("leaf_sums"):
-            _lib.call("rfxc_leaf_sums", _lib.ptr(self.perm), _lib.ptr(self.seg), 0,
-                      d.total_leaves, _lib.ptr(X32), kk, self.ld, _lib.ptr(self.S),
-                      _lib.stream_handle())
-        with region("leaf_gather"):
-            _lib.call("rfxc_leaf_gather", _lib.ptr(d.codes_nb), d.n, d.Bl, _lib.ptr(d.leaf_base),
-                      _lib.ptr(self.S), kk, self.ld, 1.0 / d.B, 0, _lib.ptr(Y),
-                      _lib.stream_handle())
+        if self.fused:
+            if kk != self.k:
+                # fewer surviving columns: the padded operand keeps stride ld,
+                # so sketch all ld columns and keep the first kk
+                full = torch.empty((d.n, self.k), dtype=torch.float64, device=X32.device)
+                self._pass(X32, full)
+                Y.copy_(full[:, :kk])
+            else:
+                self._pass(X32, Y)
+        else:
+            with region("leaf_sums"):
+                _lib.call("rfxc_leaf_sums", _lib.ptr(self.perm), _lib.ptr(self.seg), 0,
+                          d.total_leaves, _lib.ptr(X32), kk, self.ld, _lib.ptr(self.S),
+                          _lib.stream_handle())
+            with region("leaf_gather"):
+                _lib.call("rfxc_leaf_gather", _lib.ptr(d.codes_nb), d.n, d.Bl,
+                          _lib.ptr(d.leaf_base), _lib.ptr(self.S), kk, self.ld, 1.0 / d.B, 0,
+                          _lib.ptr(Y), _lib.stream_handle())
         if d.is_shard and reduce:
             import torch.distributed as dist
             dist.all_reduce(Y, op=dist.ReduceOp.SUM, group=self.group)
         return Y
+
+    def _pass(self, X32, Y):
+        d = self.d
+        with region("sketch_pass"):
+            _lib.call("rfxc_sketch_pass", _lib.ptr(self.perm), _lib.ptr(self.seg),
+                      _lib.ptr(d.codes_nb), _lib.ptr(d.leaf_base), _lib.ptr(d.has_empty), d.n,
+                      d.Bl, _lib.ptr(X32), self.k, self.ld, 1.0 / d.B, self.T, self.s_rows,
+                      _lib.ptr(Y), _lib.ptr(self.work), _lib.stream_handle())
 
 
 def _gram(A, Bm):

@@ -20,6 +20,10 @@ for rep in range(2):
     nb, tm, _ = traverse(df, dv)
     dm = DeviceMembership(nb, tm, df.leaf_counts, 0, B, B)
     sk = P._Sketch(dm, 40)
+    if rep == 0:
+        lc = dm.leaf_counts
+        print("has_empty", int(dm.has_empty.item()), "T", getattr(sk, "T", None), "s_rows",
+              getattr(sk, "s_rows", None), "leaves/tree", lc.mean(), lc.max(), flush=True)
     X32 = torch.randn((ds.n, sk.ld), dtype=torch.float32, device="cuda")
     sk.apply(X32, 40)
 torch.cuda.synchronize()

@@ -133,4 +133,6 @@ def test_tree_shard_sum_equals_whole(synth2k):
     Yw = P._Sketch(P.leaf_membership(forest, ds).device(), k).apply(X32, k)
     Ys = sum(P._Sketch(P.leaf_membership(forest, ds, trees=t).device(), k)
              .apply(X32, k, reduce=False) for t in [(0, 13), (13, 31), (31, 40)])
-    assert torch.allclose(Ys, Yw, rtol=1e-12, atol=1e-12)
+    # per-batch f32 partial sums (rfxc_sketch_pass): shard boundaries change
+    # the batching, so agreement is to f32 rounding of the batch partials
+    assert torch.allclose(Ys, Yw, rtol=1e-6, atol=1e-6 * float(Yw.abs().max()))

@@ -116,9 +116,14 @@ def test_bucket_is_stable_counting_sort(synth2k):
     perm, seg = perm.cpu().numpy(), seg.cpu().numpy()
     codes = golden("synth2k.npz")["codes"]
     n = codes.shape[0]
+    first = (perm.view(np.uint32) >> 31).astype(bool)
+    perm = perm & 0x7FFFFFFF
     for b in (0, 7, 39):
         want = np.argsort(codes[:, b], kind="stable")
         assert np.array_equal(perm[b], want)
+        # RFXC_PERM_FIRST marks exactly the first member of every leaf
+        sc = codes[want, b]
+        assert np.array_equal(first[b], np.r_[True, sc[1:] != sc[:-1]])
         lo, hi = d.leaf_base_host[b], d.leaf_base_host[b + 1]
         starts = seg[lo:hi + 1] - b * n
         assert np.array_equal(np.diff(starts), np.bincount(codes[:, b], minlength=hi - lo))
