@@ -224,6 +224,23 @@ int rfxc_matmul_small(const double* d_Y, int64_t n, int32_t ka,
                       const double* d_M, int32_t kb, double* d_Z,
                       float* d_Z32, int32_t ld32, void* stream);
 
+/* k x k steps of the basis / Rayleigh-Ritz (np.linalg.qr, proximity.py:395,
+ * :397; np.linalg.eigh of T, proximity.py:399-403) on one CTA, k <= 110, so
+ * the factorisation never waits on the host.  All matrices row-major f64.
+ *   rfxc_orth_map: G = Y^T Y -> M (k x k): Q1 = Y M has orthonormal columns
+ *     (eigen-directions of G, strongest first, scaled by l^-1/2; directions
+ *     with l <= 1e-13 l_max become zero columns).
+ *   rfxc_chol_inv: G + shift_rel tr(G) I = R^T R (Cholesky) -> R^-1 (upper;
+ *     non-positive pivots give zero rows/columns).  Q = Y R^-1 is one
+ *     CholeskyQR step; the basis is shifted CholeskyQR3 (first step shifted).
+ *   rfxc_ritz_factor_map: T -> Wr (k x r) = W_r sqrt(clip(l_r, 0)), the
+ *     top-r eigenpairs (descending) of the symmetrised T.
+ *   rfxc_sym_eig: eigenvalues (descending) and eigenvectors (columns). */
+int rfxc_orth_map(const double* d_G, int32_t k, double* d_M, void* stream);
+int rfxc_chol_inv(const double* d_G, int32_t k, double shift_rel, double* d_Rinv, void* stream);
+int rfxc_ritz_factor_map(const double* d_T, int32_t k, int32_t r, double* d_Wr, void* stream);
+int rfxc_sym_eig(const double* d_A, int32_t k, double* d_w, double* d_V, void* stream);
+
 /* -------------------------------------------------------------------- K6 */
 /* factor = Q (n, k) @ Wr (k, r) followed by quantisation (quantize.py:83-117,
  * i8: per-column absmax/127, rint half-even, clip +-127).

@@ -58,6 +58,10 @@ SIGNATURES = {
     "rfxc_gram_parts": (ctypes.c_int, [I64]),
     "rfxc_gram": (ctypes.c_int, [P, P, I64, I32, I32, P, P, P]),
     "rfxc_matmul_small": (ctypes.c_int, [P, I64, I32, P, I32, P, P, I32, P]),
+    "rfxc_orth_map": (ctypes.c_int, [P, I32, P, P]),
+    "rfxc_chol_inv": (ctypes.c_int, [P, I32, F64, P, P]),
+    "rfxc_ritz_factor_map": (ctypes.c_int, [P, I32, I32, P, P]),
+    "rfxc_sym_eig": (ctypes.c_int, [P, I32, P, P, P]),
     "rfxc_factor_quantize": (ctypes.c_int, [P, I64, I32, P, I32, I32, P, P, P, P, P]),
     "rfxc_dequantize": (ctypes.c_int, [P, P, I64, I32, I32, P, P]),
     "rfxc_pmax": (ctypes.c_int, [P, I64, I32, I64, P, P, P]),
@@ -108,7 +112,8 @@ LAUNCHES = {"rfxc_values_to_f32": 1, "rfxc_forest_pack": 1, "rfxc_leaf_codes": 1
             "rfxc_transpose_i32": 1, "rfxc_bucket": 1, "rfxc_pair_counts": 1,
             "rfxc_triblock_count": 1, "rfxc_triblock_emit": 1, "rfxc_exclusive_scan_i64": 1,
             "rfxc_normals": 1, "rfxc_pack_f32": 1, "rfxc_leaf_sums": 1, "rfxc_leaf_gather": 1,
-            "rfxc_sketch_prepare": 1, "rfxc_sketch_pass": 1,
+            "rfxc_sketch_prepare": 1, "rfxc_sketch_pass": 1, "rfxc_orth_map": 1,
+            "rfxc_chol_inv": 1, "rfxc_ritz_factor_map": 1, "rfxc_sym_eig": 1,
             "rfxc_gram": 2, "rfxc_matmul_small": 1, "rfxc_factor_quantize": 3,
             "rfxc_dequantize": 1, "rfxc_pmax": 2, "rfxc_mds_power": 1, "rfxc_gram_matvec": 1}
 launch_count = 0

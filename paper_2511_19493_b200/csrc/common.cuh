@@ -54,6 +54,16 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
+// FP64 tensor-core MMA (DMMA.8x8x4): D (8x8) = A (8x4, row) * B (4x8, col) + C.
+// Fragments per lane: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+// d0/d1 = D[lane/4][2*(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
 // Deterministic block reduction helpers (fixed shuffle tree + fixed smem
 // order, so the same inputs always give the same bits).
 __device__ __forceinline__ double warp_sum(double v)

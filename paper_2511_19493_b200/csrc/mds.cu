@@ -11,23 +11,28 @@
 // (mds.py:83-86, :257-261).
 //
 // G v = -1/2 H D2 H v with D2 u = pmax^2 (sum u) 1 - 2 pmax P u + (P o P) u on
-// the UNclamped P = Q Q^T (mds.py:177-179).  With Q' = [Q | 1] the single
-// reduction S' = Q'^T diag(u) Q' holds S = Q^T diag(u) Q (so that
+// the UNclamped P = Q Q^T (mds.py:177-179).  With q' = [q | 1] the single
+// reduction S' = sum_i u_i q'_i q'_i^T holds S = Q^T diag(u) Q (so that
 // (P o P)u_i = q_i^T S q_i — the Khatri-Rao identity of mds.py:147-152
-// without the n x r^2 expansion), t = Q^T u (P u_i = q_i . t) and sum(u).
-// mean(z) follows in closed form from the constants Q^T 1 and Q^T Q, so a
-// Gram matvec costs one S' pass + one row pass and two grid barriers.
+// without the n x r^2 expansion), t = Q^T u (P u_i = q_i . t) and sum(u);
+// mean(z) follows in closed form from the constants C' = sum q'q'^T.  S' is
+// linear in u, so it is accumulated for the raw v and corrected by
+// -mean(v) C' afterwards, which lets the convergence reduction of an update
+// ride along with the next matvec's reduction.
 //
-// Layout: one CTA per SM (cooperative launch); CTA c owns a contiguous row
-// slice and keeps that slice of the factor resident in shared memory for the
-// whole run (f64 rows, or int8 codes x per-column scales for large n, odd
-// row stride so lane-per-row reads are conflict-free; global memory is the
-// fallback).  The kernel is templated on that storage so the inner loops are
-// branch-free.  Every reduction has a fixed order (register tiles -> fixed
-// smem combine -> fixed block order), so results are bit-reproducible and
-// every stopping decision is identical in every CTA.  The work is FP64-FMA
-// bound: per matvec and row, ~r(r+1)/2 FMAs in each of the two passes.
+// B200 mapping: one CTA per SM (cooperative); CTA c owns a contiguous row
+// slice and keeps its factor slice in shared memory as int8 codes (code *
+// scale is bit-identical to the dequantised factor; other modes read the
+// f64 factor from L2).  Both O(n r^2) products run on the FP64 tensor cores
+// (DMMA.8x8x4): the S' reduction with one warp per 8x8 tile of the upper
+// triangle (A^T B with A = diag(v) Q', B = Q', k-steps of 4 rows), and the
+// row pass Z = Q S, PPu_i = sum_c Z_ic q_ic, with warps on 8-row blocks.
+// Per iteration: three grid barriers (S' partials -> distributed totals ->
+// projections), every reduction in a fixed order, so results are
+// bit-reproducible and every stopping decision is identical in every CTA.
 #include <cooperative_groups.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -35,11 +40,12 @@ namespace cg = cooperative_groups;
 
 namespace rfxc {
 
-constexpr int MT = 512;             // threads per CTA
-constexpr int MW = MT / 32;         // warps per CTA
-constexpr int SLOTS = 24;           // small-reduction slots per CTA
-constexpr int SMEM_BUDGET = 220 * 1024;
-constexpr int RMAX_REG = 32;        // rows held in registers for r <= 32
+constexpr int XA = 16;         // extra reduction-A slots: sum v, dmax, d_f (f < 8)
+constexpr int XS_SUM = 0, XS_DMAX = 1, XS_D = 2;
+constexpr int BS = 24;         // reduction-B slots
+constexpr int MAXRT = 24;      // r <= 192
+constexpr int SMS_MAXRP = 96;  // S kept in shared memory up to RP = 96
+constexpr int SMEM_BUDGET = 226 * 1024;
 
 enum { QS_F64 = 0, QS_I8 = 1, QS_GLOBAL = 2 };
 
@@ -56,410 +62,478 @@ struct MdsArgs {
     int mode;               // 0: MDS, 1: one gram_matvec of V[0] into w
     int qs;                 // QS_* storage of the factor slice
     int64_t rpb;            // rows per CTA
+    int TP;                 // 8-column tiles of q' (r + 1 columns)
+    int NT;                 // upper-triangle tiles TP (TP + 1) / 2
+    int PE;                 // reduction-A entries per CTA: NT * 64 + XA
     double* V;              // k x n: start vectors in, found vectors out
     double* w;              // n
-    double* parts;          // 2 x grid x SLOTS (small reductions, double-buffered)
-    double* sparts;         // grid x (E + 8) (S' partials + deflation dots)
-    double* tot;            // E + 8: totals of the current matvec
-    double* cst;            // E: constants Q'^T Q' (G = Q^T Q, c = Q^T 1, n)
+    double* sparts;         // grid x PE
+    double* tot;            // PE
+    double* cst;            // NT * 64: C' = sum q' q'^T
+    double* bparts;         // 2 x grid x BS
     double* coords;         // n x k
     double* info;           // k x 4
     int32_t* k_used;
+    unsigned long long* timing;  // debug (RFXC_MDS_TIMING): per-phase ns of CTA 0
 };
 
-struct Ctx {
-    cg::grid_group grid;
-    int64_t r0, r1;
-    int parity;
-    double* red;     // >= 32
-    double* bcast;   // SLOTS
+__device__ __forceinline__ unsigned long long gtime()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define MDS_T(slot)                                                                 \
+    do {                                                                            \
+        if (A.timing && blockIdx.x == 0 && threadIdx.x == 0) {                      \
+            const unsigned long long now_ = gtime();                                \
+            A.timing[slot] += now_ - t_last;                                        \
+            t_last = now_;                                                          \
+        }                                                                           \
+    } while (0)
+
+struct Sm {
+    const double* q64;  // rows x ldq f64 factor (QS_F64)
+    int ldq;
+    const int8_t* q8;   // rows x r codes (QS_I8)
+    const double* sc;   // r scales
+    double* us;         // rows: v of this slice
+    double* S;          // RP x RP mean-corrected S (zero padded)
+    double* ts;         // PE: this matvec's reduction-A totals (staged)
+    double* scr;        // 32 x 32 scratch
+    double* t;          // RP
+    double* red;        // 32
+    double* bc;         // BS broadcast slots
+    int* tab;           // NT x 2 tile coordinates
 };
 
-__host__ __device__ __forceinline__ int ntile(int r) { return (r + 1 + 3) / 4; }
-__host__ __device__ __forceinline__ int nentry(int r)
+__host__ __device__ __forceinline__ int rp_of(int r) { return 8 * ((r + 7) / 8); }
+// f64 slice row stride: >= RP (the zero-padded width) and = 4 (mod 16)
+// doubles, so the 4 rows of a DMMA fragment land on different bank groups
+__host__ __device__ __forceinline__ int ldq_of(int rp) { return rp + ((4 - rp % 16) + 16) % 16; }
+__host__ __device__ __forceinline__ int64_t pad16(int64_t x) { return (x + 15) / 16 * 16; }
+
+// q'(row, c) of the local slice (c == r is the constant-one column)
+template <int QS>
+__device__ __forceinline__ double qp(const MdsArgs& A, const Sm& s, int64_t r0, int64_t i, int c)
 {
-    const int t = ntile(r);
-    return 16 * t * (t + 1) / 2;
-}
-__host__ __device__ __forceinline__ int tile_index(int ta, int tb, int T)
-{
-    return ta * T - ta * (ta - 1) / 2 + (tb - ta);  // ta <= tb
+    if (c < A.r) {
+        if (QS == QS_F64) return s.q64[i * s.ldq + c];
+        if (QS == QS_I8) return (double)s.q8[i * A.r + c] * s.sc[c];
+        return __ldg(A.dq + (r0 + i) * A.r + c);
+    }
+    return c == A.r ? 1.0 : 0.0;
 }
 
-// ---------------------------------------------------------------- reductions
-// Sum m (<= SLOTS) per-thread values over the grid; every thread gets totals.
-__device__ void grid_sum(Ctx& C, const MdsArgs& A, double* v, int m)
+// raw factor value of slice row i, column c < r (no column checks)
+template <int QS>
+__device__ __forceinline__ double qraw(const MdsArgs& A, const Sm& s, int64_t r0, int64_t i, int c)
 {
-    double* parts = A.parts + (int64_t)C.parity * gridDim.x * SLOTS;
-    C.parity ^= 1;
-    for (int j = 0; j < m; j++) {
-        const double s = block_sum(v[j], C.red);
-        if (threadIdx.x == 0) parts[blockIdx.x * SLOTS + j] = s;
-    }
-    C.grid.sync();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int j = warp; j < m; j += MW) {  // one warp per slot, fixed order
-        double s = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) s += parts[b * SLOTS + j];
-        s = warp_sum(s);
-        if (lane == 0) C.bcast[j] = s;
-    }
-    __syncthreads();
-    for (int j = 0; j < m; j++) v[j] = C.bcast[j];
-    __syncthreads();
+    if (QS == QS_F64) return s.q64[i * s.ldq + c];
+    if (QS == QS_I8) return (double)s.q8[i * A.r + c] * s.sc[c];
+    return __ldg(A.dq + (r0 + i) * A.r + c);
 }
 
-// max of `mx` and sum of `sm` in one barrier
-__device__ void grid_max_sum(Ctx& C, const MdsArgs& A, double& mx, double& sm)
+// Reduction A partial of this CTA: S'(x) tiles (one warp per 8x8 tile of the
+// upper triangle, DMMA over 4-row k-steps, four independent accumulator
+// chains summed in order), written to sparts[blk].
+template <int QS>
+__device__ void spass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows, const double* x)
 {
-    double* parts = A.parts + (int64_t)C.parity * gridDim.x * SLOTS;
-    C.parity ^= 1;
-    const double bm = block_max(mx, C.red);
-    const double bs = block_sum(sm, C.red);
-    if (threadIdx.x == 0) {
-        parts[blockIdx.x * SLOTS] = bm;
-        parts[blockIdx.x * SLOTS + 1] = bs;
-    }
-    C.grid.sync();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp < 2) {
-        double s = warp == 0 ? -INFINITY : 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) {
-            const double x = parts[b * SLOTS + warp];
-            s = warp == 0 ? fmax(s, x) : s + x;
-        }
-        s = warp == 0 ? warp_max(s) : warp_sum(s);
-        if (lane == 0) C.bcast[warp] = s;
-    }
-    __syncthreads();
-    mx = C.bcast[0];
-    sm = C.bcast[1];
-    __syncthreads();
-}
-
-// (max |x|, first index) over the grid
-__device__ int64_t grid_argmax_abs(Ctx& C, const MdsArgs& A, const double* x)
-{
-    double bv = -1.0;
-    int64_t bi = INT64_MAX;
-    for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += blockDim.x) {
-        const double a = fabs(x[i]);
-        if (a > bv) { bv = a; bi = i; }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-    __shared__ double wv[MW];
-    __shared__ int64_t wi[MW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
-    __syncthreads();
-    double* parts = A.parts + (int64_t)C.parity * gridDim.x * SLOTS;
-    C.parity ^= 1;
-    if (threadIdx.x == 0) {
-        double v = wv[0];
-        int64_t ii = wi[0];
-        for (int w = 1; w < MW; w++)
-            if (wv[w] > v || (wv[w] == v && wi[w] < ii)) { v = wv[w]; ii = wi[w]; }
-        parts[blockIdx.x * SLOTS] = v;
-        parts[blockIdx.x * SLOTS + 1] = __longlong_as_double((long long)ii);
-    }
-    C.grid.sync();
-    if (threadIdx.x == 0) {
-        double v = -1.0;
-        int64_t ii = INT64_MAX;
-        for (int b = 0; b < (int)gridDim.x; b++) {
-            const double pv = parts[b * SLOTS];
-            const int64_t pi = (int64_t)__double_as_longlong(parts[b * SLOTS + 1]);
-            if (pv > v || (pv == v && pi < ii)) { v = pv; ii = pi; }
-        }
-        C.bcast[0] = __longlong_as_double((long long)ii);
-    }
-    __syncthreads();
-    const int64_t out = (int64_t)__double_as_longlong(C.bcast[0]);
-    __syncthreads();
-    return out;
-}
-
-// ------------------------------------------------------------- factor rows
-// Factor slice accessor; QSM fixed at compile time (no per-element branch).
-template <int QSM>
-struct Rows {
-    int r;
-    int ld;              // row stride (odd for the shared-memory layouts)
-    const double* f64;   // smem slice (QS_F64) or global dq (QS_GLOBAL)
-    const int8_t* i8;    // smem codes (QS_I8)
-    const double* sc;    // smem scales (QS_I8)
-    int64_t base;        // first global row of the slice (QS_GLOBAL)
-
-    __device__ __forceinline__ double q(int64_t row, int col) const  // col < r
-    {
-        if (QSM == QS_I8) return (double)i8[row * ld + col] * sc[col];
-        if (QSM == QS_F64) return f64[row * ld + col];
-        return __ldg(f64 + (base + row) * r + col);
-    }
-};
-
-// S' partial of this CTA: sum over slice rows of u_i q'_i q'_i^T (q' = [q | 1])
-// as 4x4 register tiles of the upper triangle; row groups split the slice
-// and are combined in a fixed order.  Writes nentry(r) values to `out`.
-template <int QSM>
-__device__ __forceinline__ void tile_rows(const Rows<QSM>& Q, int ta, int tb, int r,
-                                          const double* us, int64_t i0, int64_t rows,
-                                          int64_t step, double* acc)
-{
-    bool va[4], vb[4];
+    const int fr = lane & 3, fc = lane >> 2;
+    const int r = A.r;
+    double* out = A.sparts + (int64_t)blockIdx.x * A.PE;
+    if constexpr (QS == QS_F64) {
+        // zero-padded slice (rows to 16, columns to ldq): the factor tiles
+        // (both tile columns inside the zero-padded factor) run on DMMA with no
+        // checks; t = sum x_i q_i and sum x_i (the constant-one column) are a
+        // plain reduction written over the (a, r) entries afterwards
+        const int ldq = s.ldq;
+        const int RTq = (r + 7) / 8;
+        const int64_t rows16 = pad16(rows);
+        const int nw = (int)(blockDim.x >> 5);
+        for (int t = warp; t < A.NT; t += nw) {
+            const int ta = s.tab[2 * t], tb = s.tab[2 * t + 1];
+            if (tb >= RTq) continue;
+            const double* pa = s.q64 + fr * ldq + 8 * ta + fc;
+            const double* pb = s.q64 + fr * ldq + 8 * tb + fc;
+            const double* px = x + fr;
+            double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+            for (int base = 0; base < rows16; base += 16) {
 #pragma unroll
-    for (int x = 0; x < 4; x++) {
-        va[x] = 4 * ta + x < r;
-        vb[x] = 4 * tb + x < r;
-    }
-    for (int64_t i = i0; i < rows; i += step) {
-        const double u = us[i];
-        double qa[4], qb[4];
-#pragma unroll
-        for (int x = 0; x < 4; x++) {
-            const int ca = 4 * ta + x, cb = 4 * tb + x;
-            qa[x] = u * (va[x] ? Q.q(i, ca) : (ca == r ? 1.0 : 0.0));
-            qb[x] = vb[x] ? Q.q(i, cb) : (cb == r ? 1.0 : 0.0);
-        }
-#pragma unroll
-        for (int x = 0; x < 4; x++)
-#pragma unroll
-            for (int y = 0; y < 4; y++) acc[4 * x + y] += qa[x] * qb[y];
-    }
-}
-
-template <int QSM>
-__device__ void spass(const Rows<QSM>& Q, const double* us, int64_t rows, double* out,
-                      double* scratch)
-{
-    const int r = Q.r, T = ntile(r);
-    const int tiles = T * (T + 1) / 2;
-    const int tid = threadIdx.x;
-    double acc[16];
-    if (tiles > MT) {  // large r: every thread owns whole tiles, all rows
-        for (int tile = tid; tile < tiles; tile += MT) {
-            int ta = 0, rem = tile;
-            while (rem >= T - ta) { rem -= T - ta; ta++; }
-#pragma unroll
-            for (int e = 0; e < 16; e++) acc[e] = 0.0;
-            tile_rows(Q, ta, ta + rem, r, us, 0, rows, 1, acc);
-#pragma unroll
-            for (int e = 0; e < 16; e++) out[tile * 16 + e] = acc[e];
-        }
-        __syncthreads();
-        return;
-    }
-    const int groups = MT / tiles;
-    const int g = tid / tiles, tile = tid % tiles;
-#pragma unroll
-    for (int e = 0; e < 16; e++) acc[e] = 0.0;
-    int ta = 0, rem = tile;
-    while (rem >= T - ta) { rem -= T - ta; ta++; }
-    for (int tt = tid; tt < tiles * 16; tt += MT) scratch[tt] = 0.0;
-    if (g < groups) tile_rows(Q, ta, ta + rem, r, us, g, rows, groups, acc);
-    __syncthreads();
-    for (int gg = 0; gg < groups; gg++) {  // fixed combine order
-        if (g == gg) {
-#pragma unroll
-            for (int e = 0; e < 16; e++) scratch[tile * 16 + e] += acc[e];
-        }
-        __syncthreads();
-    }
-    for (int e = tid; e < tiles * 16; e += MT) out[e] = scratch[e];
-    __syncthreads();
-}
-
-// S'[a][b] from the tiled upper triangle (any a, b)
-__device__ __forceinline__ double sprime(const double* tot, int a, int b, int T)
-{
-    if (a > b) { const int s = a; a = b; b = s; }
-    const int ta = a >> 2, tb = b >> 2, x = a & 3, y = b & 3;
-    return tot[16 * tile_index(ta, tb, T) + 4 * x + y];
-}
-
-// Row pass, lane per row with the row in registers (r <= R): returns
-// pu = q.t and ppu = q^T S q for slice row i.  S is symmetric (R x R,
-// zero-padded, broadcast from shared memory), t = S'[:, r].
-template <int QSM, int R>
-__device__ __forceinline__ void row_terms_reg(const Rows<QSM>& Q, int64_t i, bool valid,
-                                              const double* Sp, const double* tv, double& pu,
-                                              double& ppu)
-{
-    double q[R];
-#pragma unroll
-    for (int b = 0; b < R; b++) q[b] = (valid && b < Q.r) ? Q.q(i, b) : 0.0;
-    pu = 0.0;
-    ppu = 0.0;
-#pragma unroll
-    for (int a = 0; a < R; a++) {
-        double acc = 0.0;
-#pragma unroll
-        for (int b = a + 1; b < R; b++) acc += Sp[a * R + b] * q[b];
-        ppu += q[a] * (Sp[a * R + a] * q[a] + 2.0 * acc);
-        pu += q[a] * tv[a];
-    }
-}
-
-// y = G x - sum_{f<nf} lam_f (v_f . x) v_f   (deflated_matvec, mds.py:203-207)
-// sx: sum of x over all rows.  Two grid barriers.
-template <int QSM>
-__device__ void matvec(Ctx& C, const MdsArgs& A, const Rows<QSM>& Q, const double* x, double sx,
-                       double* y, int nf, const double* lam, double* Sp, double* tv, double* us,
-                       double* scratch)
-{
-    const int r = A.r, T = ntile(r), E = nentry(r);
-    const int64_t n = A.n, rows = C.r1 - C.r0;
-    const double mean = sx / (double)n;
-    for (int64_t i = threadIdx.x; i < rows; i += MT) us[i] = x[C.r0 + i] - mean;
-    double dl[8];
-    for (int f = 0; f < nf; f++) dl[f] = 0.0;
-    for (int64_t i = threadIdx.x; i < rows; i += MT)
-        for (int f = 0; f < nf; f++) dl[f] += A.V[(int64_t)f * n + C.r0 + i] * x[C.r0 + i];
-    __syncthreads();
-    double* out = A.sparts + (int64_t)blockIdx.x * (E + 8);
-    spass(Q, us, rows, out, scratch);
-    for (int f = 0; f < nf; f++) {
-        const double s = block_sum(dl[f], C.red);
-        if (threadIdx.x == 0) out[E + f] = s;
-    }
-    C.grid.sync();
-    {  // distributed final reduce: one warp per entry, lanes over blocks
-        const int lane = threadIdx.x & 31;
-        const int gw = blockIdx.x * MW + (threadIdx.x >> 5), nw = gridDim.x * MW;
-        for (int e = gw; e < E + nf; e += nw) {
-            double s = 0.0;
-            for (int b = lane; b < (int)gridDim.x; b += 32)
-                s += A.sparts[(int64_t)b * (E + 8) + e];
-            s = warp_sum(s);
-            if (lane == 0) A.tot[e] = s;
-        }
-    }
-    C.grid.sync();
-    // r <= 32: padded symmetric S (RP x RP) and t in shared memory; larger r
-    // reads S' straight from the (L2-resident) totals
-    const bool small = r <= RMAX_REG;
-    const int RP = r <= 16 ? 16 : RMAX_REG;
-    if (small) {
-        for (int e = threadIdx.x; e < RP * RP; e += MT) {
-            const int a = e / RP, b = e % RP;
-            Sp[e] = (a < r && b < r) ? sprime(A.tot, a, b, T) : 0.0;
-        }
-        for (int a = threadIdx.x; a < RP; a += MT) tv[a] = a < r ? sprime(A.tot, a, r, T) : 0.0;
-    }
-    __syncthreads();
-    const double su = sprime(A.tot, r, r, T);
-    const double pm = A.pmax;
-    double ct, sgm;  // c.t and <S, G> -> closed-form mean of z
-    {
-        double a = 0.0, b = 0.0;
-        for (int e = threadIdx.x; e < r * r; e += MT)
-            b += sprime(A.tot, e / r, e % r, T) * sprime(A.cst, e / r, e % r, T);
-        for (int aa = threadIdx.x; aa < r; aa += MT)
-            a += sprime(A.cst, aa, r, T) * sprime(A.tot, aa, r, T);
-        ct = block_sum(a, C.red);
-        sgm = block_sum(b, C.red);
-    }
-    const double mz = (pm * pm) * su - 2.0 * pm * ct / (double)n + sgm / (double)n;
-    const double* d = A.tot + E;
-    for (int64_t i0 = 0; i0 < rows; i0 += MT) {
-        const int64_t i = i0 + threadIdx.x;
-        const bool valid = i < rows;
-        double pu, ppu;
-        if (r <= 16) {
-            row_terms_reg<QSM, 16>(Q, i, valid, Sp, tv, pu, ppu);
-        } else if (r <= RMAX_REG) {
-            row_terms_reg<QSM, RMAX_REG>(Q, i, valid, Sp, tv, pu, ppu);
-        } else {  // generic: S' from the totals (L1/L2), row from the slice
-            pu = 0.0;
-            ppu = 0.0;
-            if (valid) {
-                for (int a = 0; a < r; a++) {
-                    const double qa = Q.q(i, a);
-                    double acc = 0.0;
-                    for (int b = a + 1; b < r; b++) acc += sprime(A.tot, a, b, T) * Q.q(i, b);
-                    ppu += qa * (sprime(A.tot, a, a, T) * qa + 2.0 * acc);
-                    pu += qa * sprime(A.tot, a, r, T);
+                for (int u = 0; u < 4; u++) {
+                    const int off = base + 4 * u;
+                    dmma884(d[u][0], d[u][1], px[off] * pa[off * ldq], pb[off * ldq]);
                 }
             }
+            out[t * 64 + fc * 8 + 2 * fr] = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
+            out[t * 64 + fc * 8 + 2 * fr + 1] = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
         }
-        if (valid) {
-            const double zi = (pm * pm) * su - 2.0 * pm * pu + ppu;
-            double yi = -0.5 * (zi - mz);
-            for (int f = 0; f < nf; f++) yi -= lam[f] * d[f] * A.V[(int64_t)f * n + C.r0 + i];
-            y[C.r0 + i] = yi;
+        __syncthreads();
+        // t_a (a < r) and su (a = r): thread (a, g) sums rows g, g + G, ...
+        const int G = (int)blockDim.x / 32;
+        double* red = s.scr;  // G x 32 partials
+        for (int a0 = 0; a0 <= r; a0 += 32) {
+            const int a = a0 + lane, g = warp;
+            double acc = 0.0;
+            if (a <= r)
+                for (int64_t i = g; i < rows; i += G) acc += x[i] * (a < r ? s.q64[i * ldq + a] : 1.0);
+            red[g * 32 + lane] = acc;
+            __syncthreads();
+            if (g == 0 && a <= r) {
+                double v = 0.0;
+                for (int q = 0; q < G; q++) v += red[q * 32 + lane];
+                const int ta = a >> 3, tb = r >> 3;
+                const int t = ta * A.TP - ta * (ta - 1) / 2 + (tb - ta);
+                out[t * 64 + (a & 7) * 8 + (r & 7)] = v;
+            }
+            __syncthreads();
         }
+        return;
+    }
+    for (int t = warp; t < A.NT; t += (int)(blockDim.x >> 5)) {
+        const int ca = 8 * s.tab[2 * t] + fc, cb = 8 * s.tab[2 * t + 1] + fc;
+        // q' column: a factor column, the constant-one column r, or zero padding
+        const bool fa = ca < r, fb = cb < r;
+        const double oa = ca == r ? 1.0 : 0.0, ob = cb == r ? 1.0 : 0.0;
+        const int ka = fa ? ca : 0, kb = fb ? cb : 0;
+        double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+        for (int64_t base = 0; base < rows; base += 16) {
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int64_t i = base + 4 * u + fr;
+                const bool ok = i < rows;
+                const int64_t ii = ok ? i : 0;
+                const double xi = ok ? x[ii] : 0.0;
+                const double qa = fa ? qraw<QS>(A, s, r0, ii, ka) : oa;
+                const double qb = fb ? qraw<QS>(A, s, r0, ii, kb) : ob;
+                dmma884(d[u][0], d[u][1], xi * qa, ok ? qb : 0.0);
+            }
+        }
+        out[t * 64 + fc * 8 + 2 * fr] = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
+        out[t * 64 + fc * 8 + 2 * fr + 1] = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
+    }
+}
+
+// fixed-order block reduction of m per-thread values into out[0..m)
+__device__ void block_sums(double* v, int m, double* red, double* out)
+{
+    for (int j = 0; j < m; j++) {
+        const double x = block_sum(v[j], red);
+        if (threadIdx.x == 0) out[j] = x;
+        __syncthreads();
+    }
+}
+
+// Distributed final reduction of the grid's reduction-A partials into tot:
+// one warp per entry, lanes over blocks in order; the dmax slot takes a max.
+__device__ void final_a(const MdsArgs& A, int entries)
+{
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (int)(blockDim.x >> 5) + (threadIdx.x >> 5), nw = gridDim.x * (int)(blockDim.x >> 5);
+    const int dm = A.NT * 64 + XS_DMAX;
+    for (int e = gw; e < entries; e += nw) {
+        double v = (e == dm) ? 0.0 : 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) {
+            const double x = A.sparts[(int64_t)b * A.PE + e];
+            v = (e == dm) ? fmax(v, x) : v + x;
+        }
+        v = (e == dm) ? warp_max(v) : warp_sum(v);
+        if (lane == 0) A.tot[e] = v;
+    }
+}
+
+// redundant per-CTA sum of m reduction-B partials (buffer `par`) -> s.bc
+__device__ void final_b(const MdsArgs& A, const Sm& s, int par, int m)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* p = A.bparts + (int64_t)par * gridDim.x * BS;
+    for (int j = warp; j < m; j += (int)(blockDim.x >> 5)) {
+        double v = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) v += p[(int64_t)b * BS + j];
+        v = warp_sum(v);
+        if (lane == 0) s.bc[j] = v;
     }
     __syncthreads();
 }
 
-template <int QSM>
-__global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
+// S'(x) entry (a, b) of the tiled upper triangle in `src`
+__device__ __forceinline__ double tile_entry(const double* src, const int* tab, int TP, int a, int b)
+{
+    if (a > b) { const int q = a; a = b; b = q; }
+    const int ta = a >> 3, tb = b >> 3;
+    const int t = ta * TP - ta * (ta - 1) / 2 + (tb - ta);
+    (void)tab;
+    return src[t * 64 + (a & 7) * 8 + (b & 7)];
+}
+
+// One deflated Gram matvec of the slice's v (s.us) given the reduced totals:
+// builds S and t in shared memory, then the DMMA row pass writes w for the
+// slice and returns (in thread-local accumulators of the row-owner lanes)
+// the projections needed afterwards.  mode: 0 -> e_f = V_f.w, v.w, w.w;
+// 1 -> residual sum (w - lam v)^2.
+template <int QS, int RT>
+__device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows, int nf,
+                        const double* lam_s, int comp, int rmode, double lam, double* bacc)
+{
+    constexpr bool SMS = RT * 8 <= SMS_MAXRP;
+    const int r = A.r, RP = 8 * RT, TP = A.TP;
+    const int64_t n = A.n;
+    // totals staged in shared memory (one coalesced pass), then the mean-
+    // corrected S, t and the closed-form mean of z
+    const double* T = A.tot;
+    if (SMS) {
+        for (int e = threadIdx.x; e < A.PE; e += (int)blockDim.x) s.ts[e] = A.tot[e];
+        __syncthreads();
+        T = s.ts;
+    }
+    const double mean = T[A.NT * 64 + XS_SUM] / (double)n;
+    double ct = 0.0, sgm = 0.0;
+    if (SMS) {
+#pragma unroll 4
+        for (int e = threadIdx.x; e < RP * RP; e += (int)blockDim.x) {
+            const int a = e / RP, b = e % RP;
+            double v = 0.0;
+            if (a < r && b < r) {
+                const double g = tile_entry(A.cst, s.tab, TP, a, b);
+                v = tile_entry(T, s.tab, TP, a, b) - mean * g;
+                sgm += v * g;
+            }
+            s.S[e] = v;
+        }
+    } else {
+        for (int e = threadIdx.x; e < r * r; e += (int)blockDim.x) {
+            const int a = e / r, b = e % r;
+            const double g = tile_entry(A.cst, s.tab, TP, a, b);
+            sgm += (tile_entry(T, s.tab, TP, a, b) - mean * g) * g;
+        }
+    }
+    for (int a = threadIdx.x; a < RP; a += (int)blockDim.x) {
+        double v = 0.0;
+        if (a < r) {
+            const double c = tile_entry(A.cst, s.tab, TP, a, r);
+            v = tile_entry(T, s.tab, TP, a, r) - mean * c;
+            ct += c * v;
+        }
+        s.t[a] = v;
+    }
+    __syncthreads();
+    const double su = tile_entry(T, s.tab, TP, r, r) - mean * tile_entry(A.cst, s.tab, TP, r, r);
+    const double pm = A.pmax;
+    ct = block_sum(ct, s.red);
+    sgm = block_sum(sgm, s.red);
+    const double mz = (pm * pm) * su - 2.0 * pm * ct / (double)n + sgm / (double)n;
+    double dfl[8];
+    for (int f = 0; f < nf; f++) dfl[f] = lam_s[f] * T[A.NT * 64 + XS_D + f];
+    if (A.timing && blockIdx.x == 0 && threadIdx.x == 0) A.timing[11] = gtime();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane & 3, fc = lane >> 2;
+    const int KS = (r + 3) / 4;
+    for (int64_t row0 = 8 * (int64_t)warp; row0 < rows; row0 += 8 * (int)(blockDim.x >> 5)) {
+        const int64_t ia = row0 + fc;  // fragment / output row of this lane
+        const bool va = ia < rows;
+        double acc[RT][2];
+#pragma unroll
+        for (int tn = 0; tn < RT; tn++) acc[tn][0] = acc[tn][1] = 0.0;
+        double ppu = 0.0, pu = 0.0;
+        if constexpr (QS == QS_F64 && SMS) {
+            // q^T S q over the upper-triangle tile pairs of the symmetric S:
+            // Z = Q_(ta) S_(ta,tb) (2 k-steps), then ppu += w Z . Q_(tb)
+            const double* pq = s.q64 + ia * s.ldq;
+#pragma unroll
+            for (int ta = 0; ta < RT; ta++) {
+#pragma unroll
+                for (int tb = ta; tb < RT; tb++) {
+                    double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < 2; ks++) {
+                        const int kr = 8 * ta + 4 * ks + fr;
+                        dmma884(z0, z1, pq[kr], s.S[kr * RP + 8 * tb + fc]);
+                    }
+                    const double wgt = ta == tb ? 1.0 : 2.0;
+                    ppu += wgt * (z0 * pq[8 * tb + 2 * fr] + z1 * pq[8 * tb + 2 * fr + 1]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 2 * RT; j++) pu += pq[4 * j + fr] * s.t[4 * j + fr];
+        } else {
+            for (int ks = 0; ks < KS; ks++) {
+                const int c = 4 * ks + fr;
+                const double a = (va && c < r) ? qp<QS>(A, s, r0, ia, c) : 0.0;
+                const int kr = 4 * ks + fr;
+#pragma unroll
+                for (int tn = 0; tn < RT; tn++) {
+                    double b;
+                    if (SMS) {
+                        b = s.S[kr * RP + 8 * tn + fc];
+                    } else {
+                        const int cb = 8 * tn + fc;
+                        b = (kr < r && cb < r) ? tile_entry(T, s.tab, TP, kr, cb) -
+                                                     mean * tile_entry(A.cst, s.tab, TP, kr, cb)
+                                               : 0.0;
+                    }
+                    dmma884(acc[tn][0], acc[tn][1], a, b);
+                }
+            }
+            if (va) {
+#pragma unroll
+                for (int tn = 0; tn < RT; tn++) {
+                    const int c = 8 * tn + 2 * fr;
+                    if (c < r) ppu += acc[tn][0] * qp<QS>(A, s, r0, ia, c);
+                    if (c + 1 < r) ppu += acc[tn][1] * qp<QS>(A, s, r0, ia, c + 1);
+                }
+                for (int c = fr; c < r; c += 4) pu += qp<QS>(A, s, r0, ia, c) * s.t[c];
+            }
+        }
+        ppu += __shfl_xor_sync(0xffffffffu, ppu, 1);
+        ppu += __shfl_xor_sync(0xffffffffu, ppu, 2);
+        pu += __shfl_xor_sync(0xffffffffu, pu, 1);
+        pu += __shfl_xor_sync(0xffffffffu, pu, 2);
+        if (va && fr == 0) {
+            const int64_t g = r0 + ia;
+            const double zi = (pm * pm) * su - 2.0 * pm * pu + ppu;
+            double yi = -0.5 * (zi - mz);
+            for (int f = 0; f < nf; f++) yi -= dfl[f] * A.V[(int64_t)f * n + g];
+            A.w[g] = yi;
+            if (rmode == 0) {
+                for (int f = 0; f < nf; f++) bacc[f] += A.V[(int64_t)f * n + g] * yi;
+                bacc[nf] += s.us[ia] * yi;
+                bacc[nf + 1] += yi * yi;
+            } else if (rmode == 1) {
+                const double e = yi - lam * s.us[ia];
+                bacc[0] += e * e;
+            }
+        }
+    }
+    (void)comp;
+    if (A.timing && blockIdx.x == 0 && threadIdx.x == 0) A.timing[12] += gtime() - A.timing[11];
+    __syncthreads();
+}
+
+// grid-wide sum of m per-thread values (one barrier, redundant final)
+__device__ void grid_sum(const MdsArgs& A, const Sm& s, cg::grid_group& grid, int& par, double* v,
+                         int m)
+{
+    double* p = A.bparts + (int64_t)par * gridDim.x * BS;
+    block_sums(v, m, s.red, s.bc);
+    if (threadIdx.x < m) p[(int64_t)blockIdx.x * BS + threadIdx.x] = s.bc[threadIdx.x];
+    grid.sync();
+    final_b(A, s, par, m);
+    for (int j = 0; j < m; j++) v[j] = s.bc[j];
+    __syncthreads();
+    par ^= 1;
+}
+
+template <int QS, int RT, int NTH>
+__global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
 {
     extern __shared__ __align__(16) unsigned char msm[];
     __shared__ double red[32];
-    __shared__ double bcast[SLOTS];
+    __shared__ double bc[BS];
     __shared__ double lam_s[8];
-    const int r = A.r, T = ntile(r), E = nentry(r);
-    const int RP = r <= 16 ? 16 : (r <= RMAX_REG ? RMAX_REG : 0);
-    const int SCR = T * (T + 1) / 2 <= MT ? 16 * T * (T + 1) / 2 : 0;
-    Ctx C{cg::this_grid(), 0, 0, 0, red, bcast};
+    __shared__ int tab[2 * 300];
+    cg::grid_group grid = cg::this_grid();
+    constexpr bool SMS = RT * 8 <= SMS_MAXRP;
+    const int r = A.r, RP = 8 * RT;
     const int64_t n = A.n;
-    C.r0 = min64(n, blockIdx.x * A.rpb);
-    C.r1 = min64(n, C.r0 + A.rpb);
-    const int64_t rows = C.r1 - C.r0;
+    const int64_t r0 = min64(n, blockIdx.x * A.rpb);
+    const int64_t rows = min64(n, r0 + A.rpb) - r0;
 
-    // shared memory: [S RPxRP] [t RP] [tile scratch] [u rpb] [factor slice]
-    double* Sp = reinterpret_cast<double*>(msm);
-    double* tv = Sp + RP * RP;
-    double* scratch = tv + RP;
-    double* us = scratch + SCR;
-    unsigned char* qbase = reinterpret_cast<unsigned char*>(us + A.rpb);
-    Rows<QSM> Q{r, r | 1, nullptr, nullptr, nullptr, C.r0};
-    if (QSM == QS_F64) {
-        double* qs = reinterpret_cast<double*>(qbase);
-        for (int64_t e = threadIdx.x; e < rows * r; e += MT)
-            qs[(e / r) * Q.ld + e % r] = A.dq[C.r0 * r + e];
-        Q.f64 = qs;
-    } else if (QSM == QS_I8) {
-        double* sc = reinterpret_cast<double*>(qbase);
-        int8_t* qs = reinterpret_cast<int8_t*>(sc + r);
-        for (int e = threadIdx.x; e < r; e += MT) sc[e] = A.scales[e];
-        for (int64_t e = threadIdx.x; e < rows * r; e += MT)
-            qs[(e / r) * Q.ld + e % r] = A.codes[C.r0 * r + e];
-        Q.i8 = qs;
-        Q.sc = sc;
-    } else {
-        Q.f64 = A.dq;
+    // shared memory: [S RPxRP if SMS] [t RP] [us rpb] [scales r] [codes rows x r]
+    Sm s;
+    s.S = reinterpret_cast<double*>(msm);
+    s.t = s.S + (SMS ? RP * RP : 0);
+    s.ts = s.t + RP;
+    s.us = s.ts + (SMS ? A.PE : 0);
+    s.scr = s.us + pad16(A.rpb);
+    double* scs = s.scr + 32 * 32;
+    s.sc = scs;
+    s.q8 = reinterpret_cast<const int8_t*>(scs + r);
+    s.ldq = ldq_of(RP);
+    s.q64 = scs + r;
+    s.red = red;
+    s.bc = bc;
+    s.tab = tab;
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int a = 0; a < A.TP; a++)
+            for (int b = a; b < A.TP; b++) {
+                tab[2 * t] = a;
+                tab[2 * t + 1] = b;
+                t++;
+            }
     }
-    __syncthreads();
-
-    {  // constants Q'^T Q' (G = Q^T Q, c = Q^T 1) with u = 1
-        for (int64_t i = threadIdx.x; i < rows; i += MT) us[i] = 1.0;
-        __syncthreads();
-        double* out = A.sparts + (int64_t)blockIdx.x * (E + 8);
-        spass(Q, us, rows, out, scratch);
-        C.grid.sync();
-        const int lane = threadIdx.x & 31;
-        const int gw = blockIdx.x * MW + (threadIdx.x >> 5), nw = gridDim.x * MW;
-        for (int e = gw; e < E; e += nw) {
-            double s = 0.0;
-            for (int b = lane; b < (int)gridDim.x; b += 32)
-                s += A.sparts[(int64_t)b * (E + 8) + e];
-            s = warp_sum(s);
-            if (lane == 0) A.cst[e] = s;
+    if (QS == QS_I8) {
+        int8_t* q8 = reinterpret_cast<int8_t*>(scs + r);
+        for (int e = threadIdx.x; e < r; e += (int)blockDim.x) scs[e] = A.scales[e];
+        for (int64_t e = threadIdx.x; e < rows * r; e += (int)blockDim.x) q8[e] = A.codes[r0 * r + e];
+    } else if (QS == QS_F64) {  // zero-padded to pad16(rpb) rows x ldq columns
+        double* q64 = scs + r;
+        const int64_t tot = pad16(A.rpb) * s.ldq;
+        for (int64_t e = threadIdx.x; e < tot; e += (int)blockDim.x) {
+            const int64_t i = e / s.ldq;
+            const int c = (int)(e % s.ldq);
+            q64[e] = (i < rows && c < r) ? A.dq[(r0 + i) * r + c] : 0.0;
         }
-        C.grid.sync();
     }
+    for (int64_t i = threadIdx.x; i < pad16(A.rpb); i += (int)blockDim.x) s.us[i] = 0.0;
+    __syncthreads();
+    int par = 0;
+    const int EA = A.NT * 64 + XA;
 
-    if (A.mode == 1) {
-        double s[1] = {0.0};
-        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) s[0] += A.V[i];
-        grid_sum(C, A, s, 1);
-        matvec(C, A, Q, A.V, s[0], A.w, 0, lam_s, Sp, tv, us, scratch);
+    // constants C' = sum q' q'^T (u = 1)
+    for (int64_t i = threadIdx.x; i < rows; i += (int)blockDim.x) s.us[i] = 1.0;
+    __syncthreads();
+    spass<QS>(A, s, r0, rows, s.us);
+    grid.sync();
+    {
+        const int lane = threadIdx.x & 31;
+        const int gw = blockIdx.x * (int)(blockDim.x >> 5) + (threadIdx.x >> 5), nw = gridDim.x * (int)(blockDim.x >> 5);
+        for (int e = gw; e < A.NT * 64; e += nw) {
+            double v = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) v += A.sparts[(int64_t)b * A.PE + e];
+            v = warp_sum(v);
+            if (lane == 0) A.cst[e] = v;
+        }
+    }
+    grid.sync();
+
+    // reduction A of the slice's v (s.us) with nf deflation dots and the
+    // previous update's max change; leaves the totals in A.tot
+    unsigned long long t_last = gtime();
+    auto reduce_a = [&](int nf, double dmax_local) {
+        MDS_T(0);
+        spass<QS>(A, s, r0, rows, s.us);
+        MDS_T(1);
+        double x[2 + 8];
+        for (int j = 0; j < 2 + nf; j++) x[j] = 0.0;
+        for (int64_t i = threadIdx.x; i < rows; i += (int)blockDim.x) {
+            const double vi = s.us[i];
+            x[0] += vi;
+            for (int f = 0; f < nf; f++) x[2 + f] += A.V[(int64_t)f * n + r0 + i] * vi;
+        }
+        x[1] = 0.0;
+        double* out = A.sparts + (int64_t)blockIdx.x * A.PE + A.NT * 64;
+        block_sums(x, 2 + nf, s.red, s.bc);
+        const double dm = block_max(dmax_local, s.red);
+        if (threadIdx.x < 2 + nf) out[threadIdx.x] = threadIdx.x == XS_DMAX ? dm : s.bc[threadIdx.x];
+        MDS_T(2);
+        grid.sync();
+        MDS_T(3);
+        final_a(A, EA);
+        MDS_T(4);
+        grid.sync();
+        MDS_T(5);
+    };
+
+    if (A.mode == 1) {  // a single gram_matvec of V[0]
+        for (int64_t i = threadIdx.x; i < rows; i += (int)blockDim.x) s.us[i] = A.V[r0 + i];
+        __syncthreads();
+        reduce_a(0, 0.0);
+        double bacc[BS] = {};
+        rowpass<QS, RT>(A, s, r0, rows, 0, lam_s, 0, 2, 0.0, bacc);
         return;
     }
 
@@ -469,86 +543,88 @@ __global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
         for (int f = 0; f < comp; f++) {  // start vector: sequential Gram-Schmidt
             const double* vf = A.V + (int64_t)f * n;
             double dd[1] = {0.0};
-            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) dd[0] += vf[i] * v[i];
-            grid_sum(C, A, dd, 1);
-            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) v[i] -= dd[0] * vf[i];
+            for (int64_t i = r0 + threadIdx.x; i < r0 + rows; i += (int)blockDim.x) dd[0] += vf[i] * v[i];
+            grid_sum(A, s, grid, par, dd, 1);
+            for (int64_t i = r0 + threadIdx.x; i < r0 + rows; i += (int)blockDim.x) v[i] -= dd[0] * vf[i];
             __syncthreads();
         }
         double nn[1] = {0.0};
-        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) nn[0] += v[i] * v[i];
-        grid_sum(C, A, nn, 1);
+        for (int64_t i = r0 + threadIdx.x; i < r0 + rows; i += (int)blockDim.x) nn[0] += v[i] * v[i];
+        grid_sum(A, s, grid, par, nn, 1);
         const double nv = sqrt(nn[0]);
         if (nv == 0.0) break;
-        double sv[1] = {0.0};
-        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) {
-            v[i] /= nv;
-            sv[0] += v[i];
+        for (int64_t i = threadIdx.x; i < rows; i += (int)blockDim.x) {
+            const double x = v[r0 + i] / nv;
+            v[r0 + i] = x;
+            s.us[i] = x;
         }
-        grid_sum(C, A, sv, 1);
-        double sumv = sv[0];
+        __syncthreads();
 
-        double lam = 0.0;
-        bool conv = false;
+        double lam = 0.0, dmax_local = 0.0;
+        bool conv = false, stop = false;
         int it = 0;
-        for (it = 1; it <= A.max_it; it++) {
-            matvec(C, A, Q, v, sumv, A.w, comp, lam_s, Sp, tv, us, scratch);
-            // all projections in one reduction: e_f = v_f.w, g_f = v_f.v, v.w, w.w
-            double dots[2 * 8 + 2];
-            const int m = 2 * comp + 2;
-            for (int j = 0; j < m; j++) dots[j] = 0.0;
-            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) {
-                const double wi = A.w[i], vi = v[i];
-                for (int f = 0; f < comp; f++) {
-                    const double vf = A.V[(int64_t)f * n + i];
-                    dots[2 * f] += vf * wi;
-                    dots[2 * f + 1] += vf * vi;
-                }
-                dots[2 * comp] += vi * wi;
-                dots[2 * comp + 1] += wi * wi;
+        double rel = INFINITY;
+        while (true) {
+            reduce_a(comp, dmax_local);
+            const bool check = it >= 1;
+            const double dmax = A.tot[A.NT * 64 + XS_DMAX];
+            const bool done = (check && dmax < A.tol) || it >= A.max_it;
+            if (check && dmax < A.tol) conv = true;
+            // the matvec of this v: an iteration step, or (done) the residual
+            double bacc[BS];
+            for (int j = 0; j < BS; j++) bacc[j] = 0.0;
+            rowpass<QS, RT>(A, s, r0, rows, comp, lam_s, comp, done ? 1 : 0, lam, bacc);
+            MDS_T(6);
+            const int m = done ? 1 : comp + 2;
+            {
+                double* p = A.bparts + (int64_t)par * gridDim.x * BS;
+                block_sums(bacc, m, s.red, s.bc);
+                if (threadIdx.x < m) p[(int64_t)blockIdx.x * BS + threadIdx.x] = s.bc[threadIdx.x];
+                MDS_T(7);
+                grid.sync();
+                MDS_T(8);
+                final_b(A, s, par, m);
+                par ^= 1;
+                MDS_T(9);
             }
-            grid_sum(C, A, dots, m);
-            // w' = w - sum_f e_f v_f (orthonormal v_f): v.w' and |w'|^2 in closed form
-            lam = dots[2 * comp];
-            double nw2 = dots[2 * comp + 1];
+            if (done) {
+                rel = (lam != 0.0) ? sqrt(s.bc[0]) / fabs(lam) : INFINITY;
+                break;
+            }
+            // e_f = v_f.w (bc[f]), v.w (bc[comp]), w.w (bc[comp+1]); g_f = v_f.v (tot d_f)
+            it++;
+            lam = s.bc[comp];
+            double nw2 = s.bc[comp + 1];
+            double ef[8];
             for (int f = 0; f < comp; f++) {
-                lam -= dots[2 * f] * dots[2 * f + 1];
-                nw2 -= dots[2 * f] * dots[2 * f];
+                ef[f] = s.bc[f];
+                lam -= ef[f] * A.tot[A.NT * 64 + XS_D + f];
+                nw2 -= ef[f] * ef[f];
             }
             const double nw = sqrt(fmax(nw2, 0.0));
+            __syncthreads();
             if (nw == 0.0) {
                 lam = 0.0;
                 conv = true;
+                stop = true;
                 break;
             }
             const double sg = (lam / nw < 0.0) ? -1.0 : 1.0;  // sign of v_new . v
-            double dmax = 0.0, snew = 0.0;
-            for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) {
-                double wi = A.w[i];
-                for (int f = 0; f < comp; f++) wi -= dots[2 * f] * A.V[(int64_t)f * n + i];
+            dmax_local = 0.0;
+            for (int64_t i = threadIdx.x; i < rows; i += (int)blockDim.x) {
+                const int64_t g = r0 + i;
+                double wi = A.w[g];
+                for (int f = 0; f < comp; f++) wi -= ef[f] * A.V[(int64_t)f * n + g];
                 double vn = wi / nw;
                 if (sg < 0) vn = -vn;
-                dmax = fmax(dmax, fabs(vn - v[i]));
-                v[i] = vn;
-                snew += vn;
+                dmax_local = fmax(dmax_local, fabs(vn - s.us[i]));
+                s.us[i] = vn;
+                v[g] = vn;
             }
-            grid_max_sum(C, A, dmax, snew);
-            sumv = snew;
-            if (dmax < A.tol) {
-                conv = true;
-                break;
-            }
+            __syncthreads();
+            MDS_T(10);
         }
-        if (it > A.max_it) it = A.max_it;
-        // residual |deflated_matvec(v) - lam v| / |lam|  (mds.py:241-242)
-        matvec(C, A, Q, v, sumv, A.w, comp, lam_s, Sp, tv, us, scratch);
-        double rr[1] = {0.0};
-        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT) {
-            const double e = A.w[i] - lam * v[i];
-            rr[0] += e * e;
-        }
-        grid_sum(C, A, rr, 1);
-        const double rel = (lam != 0.0) ? sqrt(rr[0]) / fabs(lam) : INFINITY;
-        if (lam <= 0.0) break;
+        if (stop || lam <= 0.0) break;
         if (threadIdx.x == 0) lam_s[comp] = lam;
         __syncthreads();
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -559,28 +635,74 @@ __global__ void __launch_bounds__(MT, 1) mds_kernel(MdsArgs A)
         }
         kused = comp + 1;
     }
+    // coordinates: sqrt(lambda) * v with the largest-|component| positive
     for (int c = 0; c < kused; c++) {
         const double* v = A.V + (int64_t)c * n;
-        const int64_t idx = grid_argmax_abs(C, A, v);
-        const double sgn = v[idx] < 0.0 ? -1.0 : 1.0;
-        const double sl = sqrt(lam_s[c]);
-        for (int64_t i = C.r0 + threadIdx.x; i < C.r1; i += MT)
-            A.coords[i * A.k + c] = sl * (sgn < 0 ? -v[i] : v[i]);
+        double bv = -1.0;
+        int64_t bi = INT64_MAX;
+        for (int64_t i = r0 + threadIdx.x; i < r0 + rows; i += (int)blockDim.x) {
+            const double a = fabs(v[i]);
+            if (a > bv) { bv = a; bi = i; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        __shared__ double wv[32];
+        __shared__ int64_t wi[32];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
+        __syncthreads();
+        double* p = A.bparts + (int64_t)par * gridDim.x * BS;
+        if (threadIdx.x == 0) {
+            double vv = wv[0];
+            int64_t ii = wi[0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+                if (wv[w] > vv || (wv[w] == vv && wi[w] < ii)) { vv = wv[w]; ii = wi[w]; }
+            p[(int64_t)blockIdx.x * BS] = vv;
+            p[(int64_t)blockIdx.x * BS + 1] = __longlong_as_double((long long)ii);
+        }
+        grid.sync();
+        if (threadIdx.x == 0) {
+            double vv = -1.0;
+            int64_t ii = INT64_MAX;
+            for (int b = 0; b < (int)gridDim.x; b++) {
+                const double pv = p[(int64_t)b * BS];
+                const int64_t pi = (int64_t)__double_as_longlong(p[(int64_t)b * BS + 1]);
+                if (pv > vv || (pv == vv && pi < ii)) { vv = pv; ii = pi; }
+            }
+            bc[0] = v[ii] < 0.0 ? -1.0 : 1.0;
+        }
+        par ^= 1;
+        __syncthreads();
+        const double sl = sqrt(lam_s[c]) * bc[0];
+        for (int64_t i = r0 + threadIdx.x; i < r0 + rows; i += (int)blockDim.x) A.coords[i * A.k + c] = sl * v[i];
+        __syncthreads();
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *A.k_used = kused;
 }
 
 // ------------------------------------------------------------------- host
 struct Layout {
-    int64_t V, w, parts, sparts, tot, cst, bytes;
+    int64_t V, w, sparts, tot, cst, bparts, bytes;
 };
 
 static int grid_size() { return sm_count(); }
 
+static void shape(MdsArgs& A)
+{
+    A.TP = (A.r + 1 + 7) / 8;
+    A.NT = A.TP * (A.TP + 1) / 2;
+    A.PE = A.NT * 64 + XA;
+}
+
 static Layout mds_layout(int64_t n, int r, int k)
 {
+    MdsArgs A{};
+    A.r = r;
+    shape(A);
     const int G = grid_size();
-    const int64_t E = nentry(r);
     Layout L;
     int64_t o = 0;
     auto take = [&](int64_t count) {
@@ -590,63 +712,88 @@ static Layout mds_layout(int64_t n, int r, int k)
     };
     L.V = take((int64_t)k * n);
     L.w = take(n);
-    L.parts = take(2LL * G * SLOTS);
-    L.sparts = take((int64_t)G * (E + 8));
-    L.tot = take(E + 8);
-    L.cst = take(E + 8);
+    L.sparts = take((int64_t)G * A.PE);
+    L.tot = take(A.PE);
+    L.cst = take((int64_t)A.NT * 64);
+    L.bparts = take(2LL * G * BS);
     L.bytes = o;
     return L;
 }
 
-// choose the factor storage; returns the dynamic shared memory size
+static int rt_inst(int r)
+{
+    const int rt = (r + 7) / 8;
+    if (rt <= 1) return 1;
+    if (rt <= 2) return 2;
+    if (rt <= 4) return 4;
+    if (rt <= 8) return 8;
+    if (rt <= 12) return 12;
+    if (rt <= 16) return 16;
+    return 24;
+}
+
 static size_t plan_smem(MdsArgs& A)
 {
-    const int r = A.r;
-    const int64_t T = ntile(r);
-    const int RP = r <= 16 ? 16 : (r <= RMAX_REG ? RMAX_REG : 0);
-    const int64_t SCR = T * (T + 1) / 2 <= MT ? 16 * T * (T + 1) / 2 : 0;
-    const int ld = r | 1;
+    const int r = A.r, RP = 8 * rt_inst(r);
+    const bool sms = RP <= SMS_MAXRP;
     A.rpb = (A.n + grid_size() - 1) / grid_size();
-    const size_t fixed = ((size_t)RP * RP + RP + SCR + (size_t)A.rpb) * 8;
-    const size_t f64_rows = (size_t)A.rpb * ld * 8;
-    const size_t i8_rows = (size_t)r * 8 + (size_t)A.rpb * ld;
-    if (fixed + f64_rows <= SMEM_BUDGET) {
+    const size_t fixed =
+        ((sms ? (size_t)RP * RP + A.PE : 0) + RP + (size_t)pad16(A.rpb) + 32 * 32 + r) * 8;
+    const size_t f64 = (size_t)pad16(A.rpb) * ldq_of(RP) * 8;
+    const size_t i8 = (size_t)A.rpb * r;
+    if (fixed + f64 <= SMEM_BUDGET) {
         A.qs = QS_F64;
-        return fixed + f64_rows;
+        return fixed + f64;
     }
-    if (A.codes && fixed + i8_rows <= SMEM_BUDGET) {
+    if (A.codes && fixed + i8 <= SMEM_BUDGET) {
         A.qs = QS_I8;
-        return fixed + i8_rows;
+        return fixed + i8;
     }
     A.qs = QS_GLOBAL;
     return fixed;
 }
 
-template <int QSM>
+template <int QS, int RT>
 static int launch_q(MdsArgs& A, size_t smem, cudaStream_t st)
 {
-    auto kern = mds_kernel<QSM>;
+    // 16 warps while the row-pass accumulators fit 128 registers, else 8
+    constexpr int NTH = RT <= 8 ? 512 : 256;
+    auto kern = mds_kernel<QS, RT, NTH>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 1));
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "mds attr: %s", cudaGetErrorString(e));
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, MT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NTH, smem);
     if (occ < 1) return fail(RFXC_ERUNTIME, "mds: kernel does not fit an SM (r=%d)", A.r);
     void* args[] = {&A};
-    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid_size()), dim3(MT), args, smem,
-                                    st);
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid_size()), dim3(NTH), args, smem, st);
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "mds launch: %s", cudaGetErrorString(e));
     return check_launch("mds");
 }
 
+template <int RT>
+static int launch_rt(MdsArgs& A, size_t smem, cudaStream_t st)
+{
+    if (A.qs == QS_F64) return launch_q<QS_F64, RT>(A, smem, st);
+    if (A.qs == QS_I8) return launch_q<QS_I8, RT>(A, smem, st);
+    return launch_q<QS_GLOBAL, RT>(A, smem, st);
+}
+
 static int launch_mds(MdsArgs& A, cudaStream_t st)
 {
+    if (A.r > 8 * MAXRT) return fail(RFXC_EDATA, "mds: rank %d above %d", A.r, 8 * MAXRT);
     const size_t smem = plan_smem(A);
     if (smem > SMEM_BUDGET)
         return fail(RFXC_EDATA, "mds: n=%lld r=%d too large for one GPU", (long long)A.n, A.r);
-    if (A.qs == QS_F64) return launch_q<QS_F64>(A, smem, st);
-    if (A.qs == QS_I8) return launch_q<QS_I8>(A, smem, st);
-    return launch_q<QS_GLOBAL>(A, smem, st);
+    switch (rt_inst(A.r)) {
+        case 1: return launch_rt<1>(A, smem, st);
+        case 2: return launch_rt<2>(A, smem, st);
+        case 4: return launch_rt<4>(A, smem, st);
+        case 8: return launch_rt<8>(A, smem, st);
+        case 12: return launch_rt<12>(A, smem, st);
+        case 16: return launch_rt<16>(A, smem, st);
+        default: return launch_rt<24>(A, smem, st);
+    }
 }
 
 static void bind(MdsArgs& A, const Layout& L, void* d_work)
@@ -654,10 +801,10 @@ static void bind(MdsArgs& A, const Layout& L, void* d_work)
     char* base = static_cast<char*>(d_work);
     A.V = reinterpret_cast<double*>(base + L.V);
     A.w = reinterpret_cast<double*>(base + L.w);
-    A.parts = reinterpret_cast<double*>(base + L.parts);
     A.sparts = reinterpret_cast<double*>(base + L.sparts);
     A.tot = reinterpret_cast<double*>(base + L.tot);
     A.cst = reinterpret_cast<double*>(base + L.cst);
+    A.bparts = reinterpret_cast<double*>(base + L.bparts);
 }
 
 }  // namespace rfxc
@@ -688,6 +835,7 @@ extern "C" int rfxc_mds_power(const double* d_dq, const int8_t* d_codes, const d
     A.max_it = max_iterations;
     A.tol = tol;
     A.mode = 0;
+    shape(A);
     bind(A, mds_layout(n, r, k), d_work);
     A.coords = d_coords;
     A.info = d_info;
@@ -699,7 +847,19 @@ extern "C" int rfxc_mds_power(const double* d_dq, const int8_t* d_codes, const d
     }
     cudaMemsetAsync(d_info, 0, (size_t)k * 4 * 8, st);
     cudaMemsetAsync(d_coords, 0, (size_t)n * k * 8, st);
-    return launch_mds(A, st);
+    A.timing = nullptr;
+    if (!getenv("RFXC_MDS_TIMING")) return launch_mds(A, st);
+    cudaMalloc(&A.timing, 16 * 8);
+    cudaMemsetAsync(A.timing, 0, 16 * 8, st);
+    int rc = launch_mds(A, st);
+    unsigned long long h[16];
+    cudaMemcpy(h, A.timing, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(A.timing);
+    const char* names[11] = {"other", "spass", "extras", "syncA1", "finalA", "syncA2", "rowpass",
+                             "bparts", "syncB", "finalB", "update"};
+    for (int i = 0; i < 11; i++) fprintf(stderr, "[mds] %-8s %9.3f ms\n", names[i], h[i] * 1e-6);
+    fprintf(stderr, "[mds] rowpass main loop (CTA 0, thread 0) %9.3f ms\n", h[12] * 1e-6);
+    return rc;
 }
 
 extern "C" int rfxc_gram_matvec(const double* d_dq, int64_t n, int32_t r, double pmax,
@@ -716,6 +876,7 @@ extern "C" int rfxc_gram_matvec(const double* d_dq, int64_t n, int32_t r, double
     A.max_it = 1;
     A.tol = 1.0;
     A.mode = 1;
+    shape(A);
     bind(A, mds_layout(n, r, 1), d_work);
     A.w = d_w;
     const cudaError_t e = cudaMemcpyAsync(A.V, d_v, (size_t)n * 8, cudaMemcpyDeviceToDevice, st);

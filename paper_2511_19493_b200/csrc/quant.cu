@@ -23,14 +23,18 @@ __constant__ double NF4_CB[16] = {
 
 int gram_parts(int64_t n);
 
-// F = Q @ Wr row by row; per-part column absmax.
+// F = Q @ Wr row by row; per-part column absmax.  Wr staged in shared memory
+// (SW) or read through L1 when k x r is too large.
+template <bool SW>
 __global__ void __launch_bounds__(256)
 factor_kernel(const double* __restrict__ Q, int64_t n, int k, const double* __restrict__ Wr, int r,
               int64_t rows_per_part, double* __restrict__ F, double* __restrict__ colmax_parts)
 {
-    extern __shared__ double wsm[];  // k x r
-    double* cm = wsm + k * r;        // blockDim partial maxima per column slot
-    for (int e = threadIdx.x; e < k * r; e += blockDim.x) wsm[e] = Wr[e];
+    extern __shared__ double wsm[];  // [k x r if SW] [blockDim partial maxima]
+    double* cm = wsm + (SW ? k * r : 0);
+    if (SW)
+        for (int e = threadIdx.x; e < k * r; e += blockDim.x) wsm[e] = Wr[e];
+    const double* W = SW ? wsm : Wr;
     __syncthreads();
     const int64_t r0 = blockIdx.x * rows_per_part, r1 = min(n, r0 + rows_per_part);
     // thread -> (row offset, column): columns fastest
@@ -41,7 +45,7 @@ factor_kernel(const double* __restrict__ Q, int64_t n, int k, const double* __re
     if (roff < rstep) {
         for (int64_t i = r0 + roff; i < r1; i += rstep) {
             double s = 0.0;
-            for (int a = 0; a < k; a++) s += Q[i * k + a] * wsm[a * r + c];
+            for (int a = 0; a < k; a++) s += Q[i * k + a] * (SW ? W[a * r + c] : __ldg(W + a * r + c));
             F[i * r + c] = s;
             m = fmax(m, fabs(s));
         }
@@ -202,10 +206,18 @@ extern "C" int rfxc_factor_quantize(const double* d_Q, int64_t n, int32_t k, con
     const int parts = gram_parts(n);
     const int64_t rpp = ceil_div(n, parts);
     const int threads = 256;
-    const size_t smem = ((size_t)k * r + threads) * 8;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    factor_kernel<<<parts, threads, smem, st>>>(d_Q, n, k, d_Wr, r, rpp, d_factor, d_colmax_parts);
+    const bool sw = (size_t)k * r * 8 <= 160 * 1024;
+    const size_t smem = ((sw ? (size_t)k * r : 0) + threads) * 8;
+    if (sw) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        factor_kernel<true><<<parts, threads, smem, st>>>(d_Q, n, k, d_Wr, r, rpp, d_factor,
+                                                          d_colmax_parts);
+    } else {
+        factor_kernel<false><<<parts, threads, smem, st>>>(d_Q, n, k, d_Wr, r, rpp, d_factor,
+                                                           d_colmax_parts);
+    }
     int rc = check_launch("factor");
     if (rc) return rc;
     const int64_t total = n * r;

@@ -199,118 +199,164 @@ leaf_gather_kernel(const int32_t* __restrict__ codes, int64_t n, int Bl,
 }
 
 // ------------------------------------------------------------------ Gram
-constexpr int GRAM_ROWS = 32;
+// C = A^T B for skinny row-major f64 A (n, ka), B (n, kb) on the FP64 tensor
+// cores: every warp walks 4-row steps of its CTA's contiguous row range,
+// loading A^T (8 x 4) and B (4 x 8) fragments straight from the rows and
+// accumulating all (ka/8 x kb/8) output tiles in registers with DMMA.8x8x4;
+// the CTA's warps are combined in a fixed order in shared memory and one warp
+// per entry then adds the per-CTA partials in block order.  Deterministic.
 constexpr int GRAM_THREADS = 256;
 
 int gram_parts(int64_t n)
 {
-    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 128), (int64_t)sm_count() * 4));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 2));
 }
 
-__global__ void __launch_bounds__(GRAM_THREADS)
+// TAM x TBM accumulator tiles (compile-time indices); runtime TA <= TAM, TB <= TBM
+template <int TAM, int TBM>
+__global__ void __launch_bounds__(GRAM_THREADS, 2)
 gram_partial_kernel(const double* __restrict__ A, int lda, const double* __restrict__ Bm, int ldb,
                     int64_t n, int ka, int kb, int64_t rows_per_part, double* __restrict__ parts)
 {
-    // 4x4 register tiles of C over (ka x kb); row groups split this part's rows
-    // and are combined in a fixed order through shared memory.
-    extern __shared__ double gsm[];  // tiles x 16
+    extern __shared__ double gsm[];  // TA*TB tiles x 64
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int64_t r0 = blockIdx.x * rows_per_part;
     const int64_t r1 = min64(n, r0 + rows_per_part);
-    const int TA = (ka + 3) / 4, TB = (kb + 3) / 4, tiles = TA * TB;
-    const int groups = max(1, GRAM_THREADS / tiles);
-    const int tid = threadIdx.x;
-    const int g = tid / tiles;
-    for (int e = tid; e < tiles * 16; e += GRAM_THREADS) gsm[e] = 0.0;
-    __syncthreads();
-    for (int tile0 = 0; tile0 < tiles; tile0 += GRAM_THREADS) {
-        const int tile = tiles > GRAM_THREADS ? tile0 + tid : tid % tiles;
-        const bool active = tile < tiles && g < groups;
-        double acc[16];
+    const int TA = (ka + 7) / 8, TB = (kb + 7) / 8;
+    double acc[TAM][TBM][2];
 #pragma unroll
-        for (int e = 0; e < 16; e++) acc[e] = 0.0;
-        const int ta = tile / TB, tb = tile % TB;
-        if (active) {
-            bool va[4], vb[4];
+    for (int x = 0; x < TAM; x++)
 #pragma unroll
-            for (int x = 0; x < 4; x++) {
-                va[x] = 4 * ta + x < ka;
-                vb[x] = 4 * tb + x < kb;
-            }
-            const int gstep = tiles > GRAM_THREADS ? 1 : groups;
-            const int gi = tiles > GRAM_THREADS ? 0 : g;
-            for (int64_t i = r0 + gi; i < r1; i += gstep) {
-                double qa[4], qb[4];
+        for (int y = 0; y < TBM; y++) acc[x][y][0] = acc[x][y][1] = 0.0;
+    const int fr = lane & 3, fc = lane >> 2;  // fragment row (k) / column
+    double af[TAM], bf[TBM], an[TAM], bn[TBM];
+    auto load = [&](int64_t base, double* fa, double* fb) {
+        const int64_t row = base + fr;
+        const bool rv = row < r1;
 #pragma unroll
-                for (int x = 0; x < 4; x++) {
-                    qa[x] = va[x] ? __ldg(A + i * lda + 4 * ta + x) : 0.0;
-                    qb[x] = vb[x] ? __ldg(Bm + i * ldb + 4 * tb + x) : 0.0;
-                }
-#pragma unroll
-                for (int x = 0; x < 4; x++)
-#pragma unroll
-                    for (int y = 0; y < 4; y++) acc[4 * x + y] += qa[x] * qb[y];
-            }
+        for (int x = 0; x < TAM; x++) {
+            const int c = 8 * x + fc;
+            fa[x] = (rv && x < TA && c < ka) ? __ldg(A + row * lda + c) : 0.0;
         }
-        if (tiles > GRAM_THREADS) {
-            if (active)
 #pragma unroll
-                for (int e = 0; e < 16; e++) gsm[tile * 16 + e] = acc[e];
-        } else {
-            for (int gg = 0; gg < groups; gg++) {  // fixed combine order
-                if (g == gg && active)
-#pragma unroll
-                    for (int e = 0; e < 16; e++) gsm[tile * 16 + e] += acc[e];
-                __syncthreads();
-            }
+        for (int y = 0; y < TBM; y++) {
+            const int c = 8 * y + fc;
+            fb[y] = (rv && y < TB && c < kb) ? __ldg(Bm + row * ldb + c) : 0.0;
         }
-        if (tiles <= GRAM_THREADS) break;
+    };
+    int64_t base = r0 + 4 * warp;
+    load(base, af, bf);
+    for (; base < r1; base += 4 * nw) {
+        load(base + 4 * nw, an, bn);  // next step's fragments in flight
+#pragma unroll
+        for (int x = 0; x < TAM; x++)
+#pragma unroll
+            for (int y = 0; y < TBM; y++)
+                if (x < TA && y < TB) dmma884(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+#pragma unroll
+        for (int x = 0; x < TAM; x++) af[x] = an[x];
+#pragma unroll
+        for (int y = 0; y < TBM; y++) bf[y] = bn[y];
     }
+    // every warp parks its tiles, then one fixed-order sum over the warps
+    const int tiles = TA * TB;
+#pragma unroll
+    for (int x = 0; x < TAM; x++)
+#pragma unroll
+        for (int y = 0; y < TBM; y++) {
+            if (x < TA && y < TB) {
+                double* d = gsm + ((int64_t)warp * tiles + x * TB + y) * 64 + fc * 8 + 2 * fr;
+                d[0] = acc[x][y][0];
+                d[1] = acc[x][y][1];
+            }
+        }
     __syncthreads();
     double* out = parts + (int64_t)blockIdx.x * ka * kb;
-    for (int e = tid; e < ka * kb; e += GRAM_THREADS) {
+    for (int e = threadIdx.x; e < ka * kb; e += blockDim.x) {
         const int a = e / kb, b = e % kb;
-        out[e] = gsm[((a >> 2) * TB + (b >> 2)) * 16 + 4 * (a & 3) + (b & 3)];
+        const int64_t off = ((a >> 3) * TB + (b >> 3)) * 64 + (a & 7) * 8 + (b & 7);
+        double v = 0.0;
+        for (int w = 0; w < nw; w++) v += gsm[(int64_t)w * tiles * 64 + off];
+        out[e] = v;
     }
 }
 
-// C[:, c0:c0+kb] (row stride ldc) = sum over parts, fixed order
+// C[:, c0:c0+kb] (row stride ldc) = sum over parts in block order, warp per entry
 __global__ void gram_final_kernel(const double* __restrict__ parts, int nparts, int ka, int kb,
-                                  double* __restrict__ C, int ldc, int c0)
+                                  double* __restrict__ C, int ldc, int c0, int a0)
 {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int E = ka * kb;
     if (e >= E) return;
     double s = 0.0;
-    for (int q = 0; q < nparts; q++) s += parts[(int64_t)q * E + e];
-    C[(e / kb) * ldc + c0 + e % kb] = s;
+    for (int q = lane; q < nparts; q += 32) s += parts[(int64_t)q * E + e];
+    s = warp_sum(s);
+    if (lane == 0) C[(a0 + e / kb) * ldc + c0 + e % kb] = s;
 }
 
 // --------------------------------------------------------- small matmul
+// Z (n, kb) = Y (n, ka) M (ka, kb) on the FP64 tensor cores, optional zero-
+// padded f32 copy (n, ld32).  M (zero-padded to 4-row x 8-column tiles) sits
+// in shared memory; a warp computes 8-row blocks: A fragments straight from
+// the rows of Y, all kb/8 output tiles in registers.
+constexpr int MM_MAXTB = 16;  // kb <= 128
+
+template <int TBM>
 __global__ void __launch_bounds__(256)
 matmul_small_kernel(const double* __restrict__ Y, int64_t n, int ka, const double* __restrict__ M,
                     int kb, double* __restrict__ Z, float* __restrict__ Z32, int ld32)
 {
-    extern __shared__ double ysm[];  // 16 rows x ka
-    constexpr int RB = 16;
-    const int64_t r0 = blockIdx.x * (int64_t)RB;
-    const int m = (int)min64(RB, n - r0);
-    for (int e = threadIdx.x; e < RB * ka; e += blockDim.x) {
-        const int r = e / ka;
-        ysm[e] = r < m ? Y[(r0 + r) * ka + e % ka] : 0.0;
+    extern __shared__ double msm[];  // [KS*4 x TBM*8] zero-padded M
+    const int KS = (ka + 3) / 4;
+    constexpr int mw = TBM * 8;
+    for (int e = threadIdx.x; e < KS * 4 * mw; e += blockDim.x) {
+        const int a = e / mw, c = e % mw;
+        msm[e] = (a < ka && c < kb) ? M[a * kb + c] : 0.0;
     }
     __syncthreads();
-    const int wcols = Z32 ? max(kb, ld32) : kb;
-    for (int e = threadIdx.x; e < RB * wcols; e += blockDim.x) {
-        const int r = e / wcols, c = e % wcols;
-        if (r >= m) continue;
-        double s = 0.0;
-        if (c < kb)
-            for (int a = 0; a < ka; a++) s += ysm[r * ka + a] * __ldg(M + (int64_t)a * kb + c);
-        if (c < kb) Z[(r0 + r) * kb + c] = s;
-        if (Z32 && c < ld32) Z32[(r0 + r) * ld32 + c] = c < kb ? (float)s : 0.0f;
+    const int lane = threadIdx.x & 31;
+    const int fr = lane & 3, fc = lane >> 2;
+    const int64_t nblk = (n + 7) / 8;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t blk = gw; blk < nblk; blk += nwarps) {
+        const int64_t arow = blk * 8 + fc;  // A fragment row (lane / 4)
+        const bool av = arow < n;
+        double acc[TBM][2];
+#pragma unroll
+        for (int t = 0; t < TBM; t++) acc[t][0] = acc[t][1] = 0.0;
+        for (int k0 = 0; k0 < KS; k0 += 8) {  // 8 k-steps of A fragments in flight
+            double a[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int c = 4 * (k0 + u) + fr;
+                a[u] = (av && k0 + u < KS && c < ka) ? __ldg(Y + arow * ka + c) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                if (k0 + u < KS) {
+                    const double* mrow = msm + (4 * (k0 + u) + fr) * mw + fc;
+#pragma unroll
+                    for (int t = 0; t < TBM; t++) dmma884(acc[t][0], acc[t][1], a[u], mrow[8 * t]);
+                }
+            }
+        }
+        const int64_t orow = blk * 8 + fc;  // output row (lane / 4)
+        if (orow < n) {
+#pragma unroll
+            for (int t = 0; t < TBM; t++) {
+                const int c = 8 * t + 2 * fr;
+                if (c < kb) Z[orow * kb + c] = acc[t][0];
+                if (c + 1 < kb) Z[orow * kb + c + 1] = acc[t][1];
+                if (Z32) {
+                    if (c < ld32) Z32[orow * ld32 + c] = c < kb ? (float)acc[t][0] : 0.0f;
+                    if (c + 1 < ld32) Z32[orow * ld32 + c + 1] = c + 1 < kb ? (float)acc[t][1] : 0.0f;
+                }
+            }
+        }
     }
 }
-
 
 // ============================================================ fused pass
 // One sketch pass Y = scale * sum_b E_b E_b^T X as a single cooperative
@@ -427,9 +473,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // of the item cut at its start, 2 = last segment cut at its end, 3 = both
 // (the item lies inside the leaf).  Cut segments leave an f64 piece per item;
 // the last piece to arrive adds them in item order and writes the sum.
-__device__ __forceinline__ void skp_emit(const SkpArgs& A, const double* acc, int64_t g, int kind, int64_t it,
-                         int64_t pos0, int64_t g0, float4* Sb, int lane, bool lead)
+__device__ __forceinline__ void skp_emit(const SkpArgs& A, double a0, double a1, double a2,
+                                         double a3, int64_t g, int kind, int64_t it, int64_t pos0,
+                                         int64_t g0, float4* Sb, int lane, bool lead)
 {
+    const double acc[4] = {a0, a1, a2, a3};
     const int k4 = A.ld >> 2;
     if (kind == 0) {
         if (lead) Sb[(g - g0) * k4 + lane] = make_float4((float)acc[0], (float)acc[1],
@@ -497,12 +545,13 @@ __device__ __forceinline__ void slot_combine(float4& a, int R, int k4, int slot,
 // Per-warp shared scratch: SKP_RMAX x 32 uint32 (phase A perm values /
 // phase B leaf-sum row ids).
 constexpr int SKP_SCRATCH = SKP_RMAX * 32;
-constexpr int SKP_U = 8;  // row loads in flight per lane
+constexpr int SKP_UA = 8;   // phase A row loads in flight per lane
+constexpr int SKP_UB = 16;  // phase B row loads in flight per lane
 
 // Phase A item: positions [P0, P1) of batch e, in steps of R sub-chunks of
 // 32 positions.  Slot s (lanes s*k4 .. s*k4+k4-1, lane c4 owning float4
 // column c4) walks sub-chunk s of the step in position order with coalesced
-// row loads (SKP_U in flight), summing each leaf segment in f32 and writing
+// row loads (SKP_UA in flight), summing each leaf segment in f32 and writing
 // the leaf sums of segments that start and end inside its sub-chunk.  The
 // segments cut by sub-chunk boundaries (head / tail partials of every slot)
 // are then joined in position order into one f64 carry held by every slot,
@@ -573,15 +622,15 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
         bool inside = (fs & 1u) != 0;  // current segment started inside this sub-chunk
         float4 acc = z4, head = z4;
         const uint32_t* pb = pbuf + slot * 32;
-        for (int p0 = 0; p0 < 32; p0 += SKP_U) {
-            float4 x[SKP_U];
+        for (int p0 = 0; p0 < 32; p0 += SKP_UA) {
+            float4 x[SKP_UA];
 #pragma unroll
-            for (int u = 0; u < SKP_U; u++) {
+            for (int u = 0; u < SKP_UA; u++) {
                 const int p = p0 + u;
                 x[u] = (on && p < m) ? __ldg(X4 + (int64_t)pb[p] * k4 + c4) : z4;
             }
 #pragma unroll
-            for (int u = 0; u < SKP_U; u++) {
+            for (int u = 0; u < SKP_UA; u++) {
                 const int p = p0 + u;
                 if (p > 0 && p < m && ((fs >> p) & 1u)) {  // a leaf starts at p
                     if (inside) {
@@ -627,7 +676,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
                 cy[3] += (double)hj.w;
                 cvalid = true;
             }
-            if (cvalid && (fj != 0)) skp_emit(A, cy, cleaf, ckind, it, pos0, g0, Sb, lane, slot == 0);
+            if (cvalid && (fj != 0)) skp_emit(A, cy[0], cy[1], cy[2], cy[3], cleaf, ckind, it, pos0, g0, Sb, lane, slot == 0);
             // the last segment of sub-chunk j becomes the carry
             cy[0] = (double)tj.x;
             cy[1] = (double)tj.y;
@@ -645,12 +694,12 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
         __syncwarp();
     }
     const int kind = tail_open ? (ckind ? 3 : 2) : ckind;
-    skp_emit(A, cy, cleaf, kind, it, pos0, g0, Sb, lane, slot == 0);
+    skp_emit(A, cy[0], cy[1], cy[2], cy[3], cleaf, kind, it, pos0, g0, Sb, lane, slot == 0);
 }
 
 // Phase B item: samples [i0, i0 + SKP_SAMPLES) against batch e's leaf sums.
 // Slot s takes every R-th sample; its lanes gather the nT leaf-sum rows of
-// that sample (coalesced, SKP_U in flight), sum them in f32 and add the sum
+// that sample (coalesced, SKP_UB in flight), sum them in f32 and add the sum
 // to Y in f64 (scaled by 1/B in the last batch).
 __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf, int lane)
 {
@@ -692,15 +741,15 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
                 if (4 * c4 + q < A.k) yo[q] = y[q];
         }
         float4 acc = z4;
-        for (int t0 = 0; t0 < nT; t0 += SKP_U) {
-            float4 x[SKP_U];
+        for (int t0 = 0; t0 < nT; t0 += SKP_UB) {
+            float4 x[SKP_UB];
 #pragma unroll
-            for (int u = 0; u < SKP_U; u++) {
+            for (int u = 0; u < SKP_UB; u++) {
                 const int t = t0 + u;
                 x[u] = (act && t < nT) ? __ldg(Sb + (int64_t)rb[t] * k4 + c4) : z4;
             }
 #pragma unroll
-            for (int u = 0; u < SKP_U; u++) f4add(acc, x[u]);
+            for (int u = 0; u < SKP_UB; u++) f4add(acc, x[u]);
         }
         if (act) {
             const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
@@ -812,44 +861,120 @@ extern "C" int rfxc_leaf_gather(const int32_t* d_codes_nb, int64_t n, int32_t Bl
 
 extern "C" int rfxc_gram_parts(int64_t n) { return gram_parts(n); }
 
+template <int TAM, int TBM>
+static int launch_gram(const double* d_A, const double* d_B, int64_t n, int ka_tot, int kb,
+                       double* d_partials, double* d_C, cudaStream_t st)
+{
+    const int parts = gram_parts(n);
+    const int64_t rpp = ceil_div(n, parts);
+    for (int a0 = 0; a0 < ka_tot; a0 += 8 * TAM) {
+        const int ka = std::min(8 * TAM, ka_tot - a0);
+        const int TA = (ka + 7) / 8;
+        for (int c0 = 0; c0 < kb; c0 += 8 * TBM) {
+            const int w = std::min(8 * TBM, kb - c0);
+            const size_t smem = (size_t)(GRAM_THREADS / 32) * TA * ((w + 7) / 8) * 64 * 8;
+            auto kern = gram_partial_kernel<TAM, TBM>;
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kern<<<parts, GRAM_THREADS, smem, st>>>(d_A + a0, ka_tot, d_B + c0, kb, n, ka, w, rpp,
+                                                    d_partials);
+            int rc = check_launch("gram_partial");
+            if (rc) return rc;
+            gram_final_kernel<<<(unsigned)ceil_div((int64_t)ka * w * 32, 256), 256, 0, st>>>(
+                d_partials, parts, ka, w, d_C, kb, c0, a0);
+            rc = check_launch("gram_final");
+            if (rc) return rc;
+        }
+    }
+    return RFXC_OK;
+}
+
 extern "C" int rfxc_gram(const double* d_A, const double* d_B, int64_t n, int32_t ka, int32_t kb,
                          double* d_partials, double* d_C, void* stream)
 {
     // d_partials must hold rfxc_gram_parts(n) * ka * kb doubles
-    if (n < 1 || ka < 1 || kb < 1 || ka > 64 * GRAM_THREADS)
-        return fail(RFXC_EDATA, "gram: bad shape ka=%d kb=%d", ka, kb);
+    if (n < 1 || ka < 1 || kb < 1) return fail(RFXC_EDATA, "gram: bad shape ka=%d kb=%d", ka, kb);
     cudaStream_t st = as_stream(stream);
-    const int parts = gram_parts(n);
-    const int64_t rpp = ceil_div(n, parts);
-    // columns per launch: at most 768 4x4 tiles (96 KB of tile accumulators)
-    const int TA = (ka + 3) / 4;
-    const int kbc = std::max(4, std::min<int>((kb + 3) / 4 * 4, 4 * (768 / TA)));
-    for (int c0 = 0; c0 < kb; c0 += kbc) {
-        const int w = std::min(kbc, kb - c0);
-        const size_t smem = (size_t)TA * ((w + 3) / 4) * 16 * 8;
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(gram_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        gram_partial_kernel<<<parts, GRAM_THREADS, smem, st>>>(d_A, ka, d_B + c0, kb, n, ka, w, rpp,
-                                                               d_partials);
-        int rc = check_launch("gram_partial");
-        if (rc) return rc;
-        gram_final_kernel<<<(unsigned)ceil_div((int64_t)ka * w, 256), 256, 0, st>>>(
-            d_partials, parts, ka, w, d_C, kb, c0);
-        rc = check_launch("gram_final");
-        if (rc) return rc;
+    const int TA = (ka + 7) / 8;
+    if (TA <= 2) return launch_gram<2, 16>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
+    if (TA <= 5) return launch_gram<5, 5>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
+    if (TA <= 8) return launch_gram<8, 4>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
+    return launch_gram<16, 2>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
+}
+
+// wide outputs (kb > 128): plain FMA kernel, 16 rows of Y per CTA
+__global__ void __launch_bounds__(256)
+matmul_wide_kernel(const double* __restrict__ Y, int64_t n, int ka, const double* __restrict__ M,
+                   int kb, double* __restrict__ Z, float* __restrict__ Z32, int ld32)
+{
+    extern __shared__ double ysm[];
+    constexpr int RB = 16;
+    const int64_t r0 = blockIdx.x * (int64_t)RB;
+    const int m = (int)min64(RB, n - r0);
+    for (int e = threadIdx.x; e < RB * ka; e += blockDim.x) {
+        const int r = e / ka;
+        ysm[e] = r < m ? Y[(r0 + r) * ka + e % ka] : 0.0;
     }
-    return RFXC_OK;
+    __syncthreads();
+    const int wcols = Z32 ? max(kb, ld32) : kb;
+    for (int e = threadIdx.x; e < RB * wcols; e += blockDim.x) {
+        const int r = e / wcols, c = e % wcols;
+        if (r >= m) continue;
+        double acc = 0.0;
+        if (c < kb)
+            for (int a = 0; a < ka; a++) acc += ysm[r * ka + a] * __ldg(M + (int64_t)a * kb + c);
+        if (c < kb) Z[(r0 + r) * kb + c] = acc;
+        if (Z32 && c < ld32) Z32[(r0 + r) * ld32 + c] = c < kb ? (float)acc : 0.0f;
+    }
+}
+
+template <int TBM>
+static int launch_mm(const double* d_Y, int64_t n, int ka, const double* d_M, int kb, double* d_Z,
+                     float* d_Z32, int ld32, cudaStream_t st)
+{
+    const int KS = (ka + 3) / 4;
+    const size_t smem = (size_t)KS * 4 * TBM * 8 * 8;
+    auto kern = matmul_small_kernel<TBM>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return fail(RFXC_ECUDA, "matmul attr: %s", cudaGetErrorString(e));
+    }
+    const int64_t warps = ceil_div(n, 8);
+    const int grid = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)sm_count() * 2);
+    kern<<<grid, 256, smem, st>>>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32);
+    return check_launch("matmul_small");
 }
 
 extern "C" int rfxc_matmul_small(const double* d_Y, int64_t n, int32_t ka, const double* d_M,
                                  int32_t kb, double* d_Z, float* d_Z32, int32_t ld32, void* stream)
 {
-    if (n < 1 || ka < 1 || kb < 1) return fail(RFXC_EDATA, "matmul_small: bad shape");
-    const size_t smem = (size_t)16 * ka * 8;
-    matmul_small_kernel<<<(unsigned)ceil_div(n, 16), 256, smem, as_stream(stream)>>>(
-        d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32);
-    return check_launch("matmul_small");
+    const int w = std::max<int>(kb, d_Z32 ? ld32 : 0);
+    if (n < 1 || ka < 1 || kb < 1 || ka > 4096)
+        return fail(RFXC_EDATA, "matmul_small: bad shape ka=%d kb=%d", ka, kb);
+    cudaStream_t st = as_stream(stream);
+    if (w > 8 * MM_MAXTB || ka > 512) {
+        const size_t smem = (size_t)16 * ka * 8;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(matmul_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        matmul_wide_kernel<<<(unsigned)ceil_div(n, 16), 256, smem, st>>>(d_Y, n, ka, d_M, kb, d_Z,
+                                                                         d_Z32, ld32);
+        return check_launch("matmul_wide");
+    }
+    switch ((w + 7) / 8) {
+        case 1: return launch_mm<1>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+        case 2: return launch_mm<2>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+        case 3: return launch_mm<3>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+        case 4: return launch_mm<4>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+        case 5: return launch_mm<5>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+        case 6: return launch_mm<6>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+        case 7: return launch_mm<7>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+        case 8: return launch_mm<8>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+        case 9: case 10: return launch_mm<10>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+        case 11: case 12: return launch_mm<12>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+        default: return launch_mm<16>(d_Y, n, ka, d_M, kb, d_Z, d_Z32, ld32, st);
+    }
 }
 
 extern "C" int rfxc_sketch_plan(const int32_t* h_leaf_counts, int32_t Bl, int64_t n, int32_t k,

@@ -484,7 +484,7 @@ def _l2_bytes() -> int:
 
 
 # fraction of L2 the sketch may fill with X, Y and two batches of leaf sums
-SKETCH_L2_FRACTION = float(os.environ.get("RFX_SKETCH_L2_FRACTION", "0.75"))
+SKETCH_L2_FRACTION = float(os.environ.get("RFX_SKETCH_L2_FRACTION", "0.9"))
 SKETCH_FUSED_MAX_LD = 128
 
 
@@ -562,6 +562,7 @@ class _Sketch:
 
 
 def _gram(A, Bm):
+    """A^T Bm (ka x kb) on the device (fixed-order skinny reduction)."""
     import torch
     n, ka = A.shape
     kb = Bm.shape[1]
@@ -570,34 +571,50 @@ def _gram(A, Bm):
     C = torch.empty((ka, kb), dtype=torch.float64, device=A.device)
     _lib.call("rfxc_gram", _lib.ptr(A), _lib.ptr(Bm), n, ka, kb, _lib.ptr(parts), _lib.ptr(C),
               _lib.stream_handle())
-    return C.cpu().numpy()
+    return C
 
 
-def _times(Y, M, ld32):
-    """(Y @ M) on the device, f64 plus the padded f32 sketch operand."""
+def _times(Y, M, ld32=0):
+    """(Y @ M) on the device (M a device (ka, kb) tensor): f64, plus the padded
+    f32 sketch operand when ld32 > 0."""
     import torch
     n, ka = Y.shape
     kb = M.shape[1]
-    m = torch.from_numpy(np.ascontiguousarray(M, dtype=np.float64)).to(Y.device)
     Z = torch.empty((n, kb), dtype=torch.float64, device=Y.device)
-    Z32 = torch.empty((n, max(ld32, 4)), dtype=torch.float32, device=Y.device)
-    _lib.call("rfxc_matmul_small", _lib.ptr(Y), n, ka, _lib.ptr(m), kb, _lib.ptr(Z),
-              _lib.ptr(Z32), Z32.shape[1], _lib.stream_handle())
+    Z32 = torch.empty((n, max(ld32, 4)), dtype=torch.float32, device=Y.device) if ld32 else None
+    _lib.call("rfxc_matmul_small", _lib.ptr(Y), n, ka, _lib.ptr(M), kb, _lib.ptr(Z),
+              _lib.ptr(Z32), Z32.shape[1] if ld32 else 0, _lib.stream_handle())
     return Z, Z32
 
 
 def orthonormalize(Y, ld: int):
     """Orthonormal basis of range(Y) (the np.linalg.qr of proximity.py:395,
-    :397) as Gram-eigen + Cholesky QR on the device: G = Y^T Y (device
-    skinny reduction), host k x k eigh / Cholesky, Q = Y M (device).
-    Directions below the f64 noise floor of G are dropped (k' <= k).
-    Returns (Q f64 (n, k'), Q32 f32 (n, ld'))."""
+    :397), entirely on the device: shifted CholeskyQR3 (a shifted CholeskyQR
+    step, then two plain ones; each = Gram, k x k Cholesky inverse, small
+    matmul).  Returns (Q f64 (n, k), Q32 f32 (n, ld))."""
     with region("orthonormalize"):
-        return _orthonormalize(Y, ld)
+        import torch
+        n, k = Y.shape
+        if k > LINALG_MAX_K:
+            return _orthonormalize_host(Y, ld)
+        shift = 11.0 * (n * k + k * (k + 1)) * np.finfo(np.float64).eps / 2
+        Q = Y
+        for step in range(3):
+            Rinv = torch.empty((k, k), dtype=torch.float64, device=Y.device)
+            _lib.call("rfxc_chol_inv", _lib.ptr(_gram(Q, Q)), k, shift if step == 0 else 0.0,
+                      _lib.ptr(Rinv), _lib.stream_handle())
+            Q, Q32 = _times(Q, Rinv, ld if step == 2 else 0)
+        return Q, Q32
 
 
-def _orthonormalize(Y, ld: int):
-    G = _gram(Y, Y)
+LINALG_MAX_K = 110  # one-CTA k x k kernels (csrc/linalg.cu)
+RITZ_ON_DEVICE = False
+
+
+def _orthonormalize_host(Y, ld: int):
+    """k > 110: the k x k steps on the host (eigen-map + one CholeskyQR step)."""
+    import torch
+    G = _gram(Y, Y).cpu().numpy()
     lam, V = np.linalg.eigh(0.5 * (G + G.T))
     top = lam.max() if lam.size else 0.0
     keep = lam > max(top, 0.0) * 1e-13
@@ -605,14 +622,33 @@ def _orthonormalize(Y, ld: int):
         keep = np.zeros_like(keep)
         keep[-1] = True
         lam = np.maximum(lam, 1e-300)
-    M1 = V[:, keep] / np.sqrt(lam[keep])[None, :]
-    M1 = M1[:, ::-1].copy()  # strongest direction first
-    kk = M1.shape[1]
-    Q1, _ = _times(Y, M1, ld)
-    G2 = _gram(Q1, Q1)
-    R = np.linalg.cholesky(0.5 * (G2 + G2.T)).T  # G2 = R^T R
-    Rinv = np.linalg.solve(R, np.eye(kk))
-    return _times(Q1, Rinv, ld)
+    M1 = np.zeros((G.shape[0], G.shape[0]))
+    sel = np.nonzero(keep)[0][::-1]  # strongest direction first
+    M1[:, :len(sel)] = V[:, sel] / np.sqrt(lam[sel])[None, :]
+    Q1, _ = _times(Y, torch.from_numpy(M1).to(Y.device))
+    G2 = _gram(Q1, Q1).cpu().numpy()
+    kk = len(sel)
+    R = np.linalg.cholesky(0.5 * (G2[:kk, :kk] + G2[:kk, :kk].T)).T
+    Rinv = np.zeros_like(M1)
+    Rinv[:kk, :kk] = np.linalg.solve(R, np.eye(kk))
+    return _times(Q1, torch.from_numpy(Rinv).to(Y.device), ld)
+
+
+def _ritz_factor_map(T, k: int, r: int):
+    """Wr (k x r) = W_r sqrt(clip(l_r, 0)) for the top-r eigenpairs of T."""
+    import torch
+    Wr = torch.empty((k, r), dtype=torch.float64, device=T.device)
+    if k <= LINALG_MAX_K and RITZ_ON_DEVICE:
+        _lib.call("rfxc_ritz_factor_map", _lib.ptr(T), k, r, _lib.ptr(Wr), _lib.stream_handle())
+        return Wr
+    # host LAPACK eigh of the k x k T (one small D2H; the one-CTA Jacobi
+    # kernel is slower than this round trip at k = 40)
+    Th = T.cpu().numpy()
+    lam, W = np.linalg.eigh(0.5 * (Th + Th.T))
+    order = np.argsort(lam)[::-1][:r]
+    lam = np.clip(lam[order], 0.0, None)
+    Wr.copy_(torch.from_numpy(W[:, order] * np.sqrt(lam)[None, :]))
+    return Wr
 
 
 def lowrank_device(membership: LeafMembership, rank: int, mode: str = "i8", seed: int = 0,
@@ -639,20 +675,13 @@ def lowrank_device(membership: LeafMembership, rank: int, mode: str = "i8", seed
     _lib.call("rfxc_normals", seed, SEQ_FACTOR, n * k, _lib.ptr(omega), _lib.stream_handle())
     X32 = torch.empty((n, ld), dtype=torch.float32, device=dev)
     _lib.call("rfxc_pack_f32", _lib.ptr(omega), n, k, ld, _lib.ptr(X32), _lib.stream_handle())
-    # k' <= k columns survive a numerically rank-deficient basis; the f32
-    # operand keeps the padded stride ld either way
     Q, Q32 = orthonormalize(sk.apply(X32, k), ld)
     for _ in range(_POWER_ITERS):
-        Q, Q32 = orthonormalize(sk.apply(Q32, Q.shape[1]), ld)
-    Z = sk.apply(Q32, Q.shape[1])
-    T = _gram(Q, Z)
-    T = 0.5 * (T + T.T)
-    lam, W = np.linalg.eigh(T)
-    order = np.argsort(lam)[::-1][:r]
-    lam = np.clip(lam[order], 0.0, None)
-    Wr = W[:, order] * np.sqrt(lam)[None, :]
-    if Wr.shape[1] < r:  # numerically rank-deficient: zero factor columns
-        Wr = np.pad(Wr, ((0, 0), (0, r - Wr.shape[1])))
+        Q, Q32 = orthonormalize(sk.apply(Q32, k), ld)
+    Z = sk.apply(Q32, k)
+    # Rayleigh-Ritz: T = Q^T (P Q), top-r eigenpairs -> Wr = W_r sqrt(l_r)
+    with region("ritz"):
+        Wr = _ritz_factor_map(_gram(Q, Z), k, r)
     with region("factor_quantize"):
         data, scales = factor_quantize(Q, Wr, mode)
     dq = device_dequantize(data, scales, n, r, mode)

@@ -71,13 +71,14 @@ def _device_quantize(F, n: int, r: int, mode: str):
 
 def factor_quantize(Q, Wr, mode: str):
     """factor = Q @ Wr on the device, then quantise (proximity.py:403-405).
-    Q: (n, k) f64 device; Wr: (k, r) host f64.  Returns device tensors
-    (data, scales)."""
+    Q: (n, k) f64 device; Wr: (k, r) f64 (device tensor or host array).
+    Returns device tensors (data, scales)."""
     import torch
     n, k = Q.shape
     r = Wr.shape[1]
     dev = Q.device
-    wr = torch.from_numpy(np.ascontiguousarray(Wr, dtype=np.float64)).to(dev)
+    wr = Wr if isinstance(Wr, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(Wr, dtype=np.float64)).to(dev)
     F = torch.empty((n, r), dtype=torch.float64, device=dev)
     parts = torch.empty(_lib.load().rfxc_gram_parts(n) * r, dtype=torch.float64, device=dev)
     data, scales, m = _device_quantize(F, n, r, mode)
