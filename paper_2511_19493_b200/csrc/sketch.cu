@@ -591,7 +591,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
 #pragma unroll
         for (int j = 0; j < SKP_RMAX; j++) {
             const int64_t q = P0 + 32 * (int64_t)(s0 + j) + lane;
-            pv[j] = (j < R && s0 + j < nsub && q < P1) ? __ldg(A.perm + q) : 0u;
+            pv[j] = (j < R && s0 + j < nsub && q < P1) ? __ldcs(A.perm + q) : 0u;  // streamed once
         }
     };
     load_pv(0);
@@ -722,7 +722,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
 #pragma unroll
         for (int j = 0; j < SKP_RMAX; j++) {
             const int64_t i = ib + j;
-            cn[j] = (j < R && i < i1 && lane < nT) ? __ldg(A.codes + i * A.Bl + b0 + lane) : 0;
+            cn[j] = (j < R && i < i1 && lane < nT) ? __ldcs(A.codes + i * A.Bl + b0 + lane) : 0;
         }
     };
     load_codes(i0);
@@ -738,7 +738,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
         if (act && !first) {
 #pragma unroll
             for (int q = 0; q < 4; q++)
-                if (4 * c4 + q < A.k) yo[q] = y[q];
+                if (4 * c4 + q < A.k) yo[q] = __ldcs(y + q);  // Y streams through L2
         }
         float4 acc = z4;
         for (int t0 = 0; t0 < nT; t0 += SKP_UB) {
@@ -757,7 +757,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
             for (int q = 0; q < 4; q++) {
                 if (4 * c4 + q < A.k) {
                     const double v = yo[q] + (double)a4[q];
-                    y[q] = last ? v * A.scale : v;
+                    __stcs(y + q, last ? v * A.scale : v);
                 }
             }
         }
@@ -1032,6 +1032,30 @@ static int launch_skp(SkpArgs& A, cudaStream_t st)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * warps, smem);
     if (occ < 1) return fail(RFXC_ERUNTIME, "sketch_pass: kernel does not fit an SM (ld=%d)", A.ld);
     void* args[] = {&A};
+    if (getenv("RFXC_L2PERSIST")) {  // experiment: pin the leaf-sum buffers in L2
+        static bool limit_set = false;
+        int dev = 0, maxp = 0, maxw = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        if (!limit_set) {
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
+            limit_set = true;
+        }
+        cudaStreamAttrValue v = {};
+        v.accessPolicyWindow.base_ptr = A.S;
+        v.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)2 * A.s_rows * A.ld * 4, (size_t)maxw);
+        v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)maxp / (float)v.accessPolicyWindow.num_bytes);
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+        static bool said = false;
+        if (!said) {
+            fprintf(stderr, "[sketch] L2 persist max %d MB window max %d MB, window %.1f MB\n",
+                    maxp >> 20, maxw >> 20, v.accessPolicyWindow.num_bytes / 1048576.0);
+            said = true;
+        }
+    }
     e = cudaLaunchCooperativeKernel((const void*)kern, dim3(sm_count() * occ), dim3(32 * warps),
                                     args, smem, st);
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "sketch_pass launch: %s", cudaGetErrorString(e));

@@ -509,8 +509,8 @@ class _Sketch:
         # every leaf non-empty (always true for a forest's own training set)
         self.fused = self.ld <= SKETCH_FUSED_MAX_LD and not int(d.has_empty.item())
         if self.fused:
-            if budget is None:  # two batches of leaf sums next to X and Y in L2
-                budget = int(SKETCH_L2_FRACTION * _l2_bytes()) - d.n * self.ld * 4 - d.n * k * 8
+            if budget is None:  # two batches of leaf sums next to X in L2 (Y streams)
+                budget = int(SKETCH_L2_FRACTION * _l2_bytes()) - d.n * self.ld * 4
                 budget = max(budget, 8 << 20)
             T, rows, wb = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
             lc = np.ascontiguousarray(d.leaf_counts, dtype=np.int32)

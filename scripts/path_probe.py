@@ -9,7 +9,8 @@ from paper_2511_19493_b200.forest import TrainConfig, train
 from paper_2511_19493_b200.device import DeviceForest, DeviceMembership, DeviceValues, traverse
 from paper_2511_19493_b200 import proximity as P
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-X, y = make_synthetic(100_000, 100, seed=0)
+N = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000
+X, y = make_synthetic(N, 100, seed=0)
 ds = from_arrays(X, y)
 t0 = time.time()
 forest = train(ds, TrainConfig(ntree=500, iseed=1), trees=(0, B))
