@@ -403,7 +403,7 @@ __host__ __device__ inline SkpLayout skp_layout(int64_t n, int Bl, int T, int ld
     const int64_t ipb = skp_items_per_batch(n, T);
     const int nb = skp_nbatch(Bl, T);
     int64_t off = 0;
-    L.S = off;         off += align256(2 * s_rows * ld * 4);
+    L.S = off;         off += align256(s_rows * ld * 4);
     L.part = off;      off += align256(2 * ipb * ld * 8);
     L.cnt = off;       off += align256(s_rows * 4);
     L.ctr = off;       off += align256(2 * (int64_t)(nb + 1) * 4);
@@ -427,8 +427,9 @@ struct SkpArgs {
     const int32_t* item_leaf;  // nbatch x ipb
     int64_t n, s_rows, ipb;
     int Bl, k, ld, T, nbatch;
+    int nbuf;                  // leaf-sum buffers (1: A(e), B(e) on one stream)
     double scale;
-    unsigned long long* timing;  // debug (RFXC_SKETCH_TIMING): per warp, per epoch work ns
+    unsigned long long* timing;  // unused
 };
 
 // item_leaf[e * ipb + it]: global leaf containing the first position of item
@@ -545,8 +546,11 @@ __device__ __forceinline__ void slot_combine(float4& a, int R, int k4, int slot,
 // Per-warp shared scratch: SKP_RMAX x 32 uint32 (phase A perm values /
 // phase B leaf-sum row ids).
 constexpr int SKP_SCRATCH = SKP_RMAX * 32;
-constexpr int SKP_UA = 8;   // phase A row loads in flight per lane
-constexpr int SKP_UB = 16;  // phase B row loads in flight per lane
+constexpr int SKP_UA = 4;
+#ifndef SKP_MINB_A
+#define SKP_MINB_A 3
+#endif   // phase A row loads in flight per lane
+constexpr int SKP_UB = 4;  // phase B row loads in flight per lane
 
 // Phase A item: positions [P0, P1) of batch e, in steps of R sub-chunks of
 // 32 positions.  Slot s (lanes s*k4 .. s*k4+k4-1, lane c4 owning float4
@@ -563,7 +567,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
     const int64_t pos0 = (int64_t)b0 * A.n, pend = (int64_t)b1 * A.n;
     const int64_t P0 = pos0 + it * SKP_ITEM, P1 = min64(P0 + SKP_ITEM, pend);
     const int64_t g0 = A.leaf_base[b0];
-    float4* Sb = reinterpret_cast<float4*>(A.S + (int64_t)(e & 1) * A.s_rows * A.ld);
+    float4* Sb = reinterpret_cast<float4*>(A.S + (int64_t)(e % A.nbuf) * A.s_rows * A.ld);
     const int k4 = A.ld >> 2;
     const int R = min(SKP_RMAX, 32 / k4);
     const int slot = lane / k4, c4 = lane - slot * k4;
@@ -706,7 +710,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
     const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
     const int nT = b1 - b0;
     const int64_t g0 = A.leaf_base[b0];
-    const float4* Sb = reinterpret_cast<const float4*>(A.S + (int64_t)(e & 1) * A.s_rows * A.ld);
+    const float4* Sb = reinterpret_cast<const float4*>(A.S + (int64_t)(e % A.nbuf) * A.s_rows * A.ld);
     const int k4 = A.ld >> 2;
     const int R = min(SKP_RMAX, 32 / k4);
     const int slot = lane / k4, c4 = lane - slot * k4;
@@ -765,42 +769,24 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
     }
 }
 
-__global__ void __launch_bounds__(256, 2) sketch_pass_kernel(SkpArgs A)
+// One phase of one tree batch per launch (A: leaf sums of batch e; B: gather
+// of batch e into Y), one item per warp; launched back to back on one stream
+// (A(0) B(0) A(1) B(1) ...), so one leaf-sum buffer suffices and each phase
+// gets its own register budget (full occupancy for the gathers).
+template <int PH>
+__global__ void __launch_bounds__(256, PH == 0 ? SKP_MINB_A : 4) sketch_phase_kernel(SkpArgs A, int e)
 {
     extern __shared__ __align__(16) uint32_t skp_smem[];
-    cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wpc = blockDim.x >> 5;
     uint32_t* scratch = skp_smem + warp * SKP_SCRATCH;
-    const int64_t wg = (int64_t)blockIdx.x * wpc + warp;
-    const int64_t nB = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
-    for (int e = 0; e <= A.nbatch; e++) {
-        int64_t nA = 0;
-        if (e < A.nbatch) {
-            const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
-            nA = ((int64_t)(b1 - b0) * A.n + SKP_ITEM - 1) / SKP_ITEM;
-        }
-        const int64_t nb = e >= 1 ? nB : 0;
-        unsigned long long t0 = 0;
-        if (A.timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        // dynamic: A items first (longer), then B items; the next index is
-        // fetched while the current item runs
-        unsigned* ctr = A.ctr + 2 * e;
-        unsigned q = 0, qn = 0;
-        if (lane == 0) q = atomicAdd(ctr, 1u);
-        q = __shfl_sync(0xffffffffu, q, 0);
-        while (q < nA + nb) {
-            if (lane == 0) qn = atomicAdd(ctr, 1u);
-            if (q < nA) skp_phase_a(A, e, q, scratch, lane);
-            else skp_phase_b(A, e - 1, q - nA, scratch, lane);
-            q = __shfl_sync(0xffffffffu, qn, 0);
-        }
-        if (A.timing && lane == 0) {
-            unsigned long long t1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            A.timing[(int64_t)e * 148 * 64 + wg] = t1 - t0;
-        }
-        grid.sync();
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (PH == 0) {
+        const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
+        const int64_t nA = ((int64_t)(b1 - b0) * A.n + SKP_ITEM - 1) / SKP_ITEM;
+        if (q < nA) skp_phase_a(A, e, q, scratch, lane);
+    } else {
+        const int64_t nB = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
+        if (q < nB) skp_phase_b(A, e, q, scratch, lane);
     }
 }
 
@@ -992,7 +978,7 @@ extern "C" int rfxc_sketch_plan(const int32_t* h_leaf_counts, int32_t Bl, int64_
             for (int b = b0; b < std::min<int>(Bl, b0 + T); b++) s += h_leaf_counts[b];
             s_rows = std::max(s_rows, s);
         }
-        if (2 * s_rows * ld * 4 <= budget_bytes || T == 1) break;
+        if (s_rows * ld * 4 <= budget_bytes || T == 1) break;
     }
     if (T_out) *T_out = T;
     if (s_rows_out) *s_rows_out = std::max<int64_t>(s_rows, 1);
@@ -1022,43 +1008,14 @@ extern "C" int rfxc_sketch_prepare(const int64_t* d_seg, const int64_t* d_leaf_b
 
 static int launch_skp(SkpArgs& A, cudaStream_t st)
 {
-    auto kern = sketch_pass_kernel;
-    const int warps = 8;
-    const size_t smem = (size_t)warps * SKP_SCRATCH * 4;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return fail(RFXC_ECUDA, "sketch_pass attr: %s", cudaGetErrorString(e));
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * warps, smem);
-    if (occ < 1) return fail(RFXC_ERUNTIME, "sketch_pass: kernel does not fit an SM (ld=%d)", A.ld);
-    void* args[] = {&A};
-    if (getenv("RFXC_L2PERSIST")) {  // experiment: pin the leaf-sum buffers in L2
-        static bool limit_set = false;
-        int dev = 0, maxp = 0, maxw = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-        if (!limit_set) {
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
-            limit_set = true;
-        }
-        cudaStreamAttrValue v = {};
-        v.accessPolicyWindow.base_ptr = A.S;
-        v.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)2 * A.s_rows * A.ld * 4, (size_t)maxw);
-        v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)maxp / (float)v.accessPolicyWindow.num_bytes);
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
-        static bool said = false;
-        if (!said) {
-            fprintf(stderr, "[sketch] L2 persist max %d MB window max %d MB, window %.1f MB\n",
-                    maxp >> 20, maxw >> 20, v.accessPolicyWindow.num_bytes / 1048576.0);
-            said = true;
-        }
+    const size_t smem = (size_t)8 * SKP_SCRATCH * 4;
+    const int64_t nB = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
+    for (int e = 0; e < A.nbatch; e++) {
+        const int b0 = e * A.T, b1 = std::min(A.Bl, b0 + A.T);
+        const int64_t nA = ((int64_t)(b1 - b0) * A.n + SKP_ITEM - 1) / SKP_ITEM;
+        sketch_phase_kernel<0><<<(unsigned)ceil_div(nA, 8), 256, smem, st>>>(A, e);
+        sketch_phase_kernel<1><<<(unsigned)ceil_div(nB, 8), 256, smem, st>>>(A, e);
     }
-    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(sm_count() * occ), dim3(32 * warps),
-                                    args, smem, st);
-    if (e != cudaSuccess) return fail(RFXC_ECUDA, "sketch_pass launch: %s", cudaGetErrorString(e));
     return check_launch("sketch_pass");
 }
 
@@ -1095,43 +1052,22 @@ extern "C" int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg,
     A.ld = ld;
     A.T = T;
     A.nbatch = skp_nbatch(Bl, T);
+    A.nbuf = 1;
     A.scale = scale;
     cudaError_t e = cudaMemsetAsync(A.ctr, 0, 2 * (size_t)(A.nbatch + 1) * 4, st);
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "sketch_pass: %s", cudaGetErrorString(e));
     A.timing = nullptr;
     if (!getenv("RFXC_SKETCH_TIMING")) return launch_skp(A, st);
-    // debug: per-warp work time per epoch, summarised on stderr (synchronous)
-    const int64_t nWk = (int64_t)sm_count() * 64;  // >= warps of any launch
-    const size_t slots = (size_t)(A.nbatch + 1) * nWk;
-    cudaMalloc(&A.timing, slots * 8);
-    cudaMemsetAsync(A.timing, 0, slots * 8, st);
+    // debug: time the pass (synchronous)
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
     int rc = launch_skp(A, st);
     cudaEventRecord(e1, st);
-    cudaStreamSynchronize(st);
+    cudaEventSynchronize(e1);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
-    std::vector<unsigned long long> h(slots);
-    cudaMemcpy(h.data(), A.timing, slots * 8, cudaMemcpyDeviceToHost);
-    cudaFree(A.timing);
-    const int64_t nW = nWk;
-    double sum_max = 0;
-    for (int ep = 0; ep <= A.nbatch; ep++) {
-        unsigned long long mx = 0, tot = 0;
-        int64_t cnt = 0;
-        for (int64_t w = 0; w < nW; w++) {
-            const unsigned long long v = h[(size_t)ep * nW + w];
-            if (v) { mx = std::max(mx, v); tot += v; cnt++; }
-        }
-        sum_max += mx * 1e-6;
-        if (ep < 3 || ep == A.nbatch)
-            fprintf(stderr, "[sketch] epoch %d: warps %lld mean %.1f us max %.1f us\n", ep,
-                    (long long)cnt, cnt ? tot / 1e3 / cnt : 0.0, mx / 1e3);
-    }
-    fprintf(stderr, "[sketch] pass %.3f ms, sum of per-epoch max work %.3f ms, T=%d epochs=%d\n",
-            ms, sum_max, A.T, A.nbatch + 1);
+    fprintf(stderr, "[sketch] pass %.3f ms, T=%d batches=%d\n", ms, A.T, A.nbatch);
     return rc;
 }
