@@ -38,7 +38,14 @@ int feature_bits(int p)
 inline float round_down_f32(double t)
 {
     float f = (float)t;
-    if ((double)f > t) f = std::nextafter(f, -INFINITY);
+    if ((double)f > t) {  // step one ulp toward -inf on the bit pattern
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        if (f > 0.0f) u -= 1;
+        else if (f < 0.0f) u += 1;
+        else u = 0x80000001u;  // just below +0: the smallest negative subnormal
+        std::memcpy(&f, &u, 4);
+    }
     return f;
 }
 

@@ -561,14 +561,15 @@ constexpr int SKP_UB = 4;  // phase B row loads in flight per lane
 // are then joined in position order into one f64 carry held by every slot,
 // which is emitted when its leaf ends (a piece when cut by the item edge).
 // Leaf ids follow from the first-member flags (no empty leaves on this path).
+template <int K4>
 __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf, int lane)
 {
     const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
     const int64_t pos0 = (int64_t)b0 * A.n, pend = (int64_t)b1 * A.n;
     const int64_t P0 = pos0 + it * SKP_ITEM, P1 = min64(P0 + SKP_ITEM, pend);
-    const int64_t g0 = A.leaf_base[b0];
+    const int g0 = (int)A.leaf_base[b0];
     float4* Sb = reinterpret_cast<float4*>(A.S + (int64_t)(e % A.nbuf) * A.s_rows * A.ld);
-    const int k4 = A.ld >> 2;
+    const int k4 = K4 ? K4 : (A.ld >> 2);  // compile-time for the common widths
     const int R = min(SKP_RMAX, 32 / k4);
     const int slot = lane / k4, c4 = lane - slot * k4;
     const bool on = slot < R;
@@ -579,16 +580,16 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
     int tail_first = 1;
     if (lane == 0 && P1 < pend) tail_first = (__ldg(A.perm + P1) & RFXC_PERM_FIRST) != 0;
     const bool tail_open = !__shfl_sync(0xffffffffu, tail_first, 0);
-    const int64_t gi = A.item_leaf[(int64_t)e * A.ipb + it];
+    const int gi = A.item_leaf[(int64_t)e * A.ipb + it];
 
     // carry: the open segment at the current position (f64, every lane holds
     // its column group), its leaf, whether it was cut at the item start and
     // whether it holds any row yet
     double cy[4] = {0.0, 0.0, 0.0, 0.0};
-    int64_t cleaf = gi;
+    int cleaf = gi;
     int ckind = 1;
     bool cvalid = false;
-    int64_t flags_before = 0;  // flagged positions in (P0, current sub-chunk start)
+    int flags_before = 0;  // flagged positions in (P0, current sub-chunk start)
 
     uint32_t pv[SKP_RMAX];
     auto load_pv = [&](int s0) {
@@ -614,7 +615,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
         // this slot's sub-chunk
         unsigned fs = 0;
         int m = 0;
-        int64_t before = flags_before;
+        int before = flags_before;
 #pragma unroll
         for (int j = 0; j < SKP_RMAX; j++) {
             const unsigned fj = (s0 == 0 && j == 0) ? (fl[j] & ~1u) : fl[j];  // P0 itself never counts
@@ -622,7 +623,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
             if (j < slot) before += __popc(fj);
         }
         const bool first_sub = (s0 == 0 && slot == 0);
-        int64_t cur = gi + before + ((fs & 1u) && !first_sub ? 1 : 0);
+        int cur = gi + before + ((fs & 1u) && !first_sub ? 1 : 0);
         bool inside = (fs & 1u) != 0;  // current segment started inside this sub-chunk
         float4 acc = z4, head = z4;
         const uint32_t* pb = pbuf + slot * 32;
@@ -631,14 +632,14 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
 #pragma unroll
             for (int u = 0; u < SKP_UA; u++) {
                 const int p = p0 + u;
-                x[u] = (on && p < m) ? __ldg(X4 + (int64_t)pb[p] * k4 + c4) : z4;
+                x[u] = (on && p < m) ? __ldg(X4 + (pb[p] * (uint32_t)k4 + c4)) : z4;
             }
 #pragma unroll
             for (int u = 0; u < SKP_UA; u++) {
                 const int p = p0 + u;
                 if (p > 0 && p < m && ((fs >> p) & 1u)) {  // a leaf starts at p
                     if (inside) {
-                        if (on) Sb[(cur - g0) * k4 + c4] = acc;
+                        if (on) Sb[(uint32_t)(cur - g0) * k4 + c4] = acc;
                     } else {
                         head = acc;
                     }
@@ -662,7 +663,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
                                           __shfl_sync(0xffffffffu, acc.y, src),
                                           __shfl_sync(0xffffffffu, acc.z, src),
                                           __shfl_sync(0xffffffffu, acc.w, src));
-            const int64_t curj = __shfl_sync(0xffffffffu, cur, j * k4);
+            const int curj = __shfl_sync(0xffffffffu, cur, j * k4);
             const unsigned fj = (s0 == 0 && j == 0) ? (fl[j] & ~1u) : fl[j];
             const bool starts = (fl[j] & 1u) != 0;
             if (fj == 0 && !starts) {  // the whole sub-chunk continues the carry
@@ -705,13 +706,14 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
 // Slot s takes every R-th sample; its lanes gather the nT leaf-sum rows of
 // that sample (coalesced, SKP_UB in flight), sum them in f32 and add the sum
 // to Y in f64 (scaled by 1/B in the last batch).
+template <int K4>
 __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf, int lane)
 {
     const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
     const int nT = b1 - b0;
     const int64_t g0 = A.leaf_base[b0];
     const float4* Sb = reinterpret_cast<const float4*>(A.S + (int64_t)(e % A.nbuf) * A.s_rows * A.ld);
-    const int k4 = A.ld >> 2;
+    const int k4 = K4 ? K4 : (A.ld >> 2);  // compile-time for the common widths
     const int R = min(SKP_RMAX, 32 / k4);
     const int slot = lane / k4, c4 = lane - slot * k4;
     const bool on = slot < R;
@@ -750,7 +752,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
 #pragma unroll
             for (int u = 0; u < SKP_UB; u++) {
                 const int t = t0 + u;
-                x[u] = (act && t < nT) ? __ldg(Sb + (int64_t)rb[t] * k4 + c4) : z4;
+                x[u] = (act && t < nT) ? __ldg(Sb + ((uint32_t)rb[t] * k4 + c4)) : z4;
             }
 #pragma unroll
             for (int u = 0; u < SKP_UB; u++) f4add(acc, x[u]);
@@ -773,7 +775,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
 // of batch e into Y), one item per warp; launched back to back on one stream
 // (A(0) B(0) A(1) B(1) ...), so one leaf-sum buffer suffices and each phase
 // gets its own register budget (full occupancy for the gathers).
-template <int PH>
+template <int PH, int K4>
 __global__ void __launch_bounds__(256, PH == 0 ? SKP_MINB_A : 4) sketch_phase_kernel(SkpArgs A, int e)
 {
     extern __shared__ __align__(16) uint32_t skp_smem[];
@@ -783,10 +785,10 @@ __global__ void __launch_bounds__(256, PH == 0 ? SKP_MINB_A : 4) sketch_phase_ke
     if (PH == 0) {
         const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
         const int64_t nA = ((int64_t)(b1 - b0) * A.n + SKP_ITEM - 1) / SKP_ITEM;
-        if (q < nA) skp_phase_a(A, e, q, scratch, lane);
+        if (q < nA) skp_phase_a<K4>(A, e, q, scratch, lane);
     } else {
         const int64_t nB = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
-        if (q < nB) skp_phase_b(A, e, q, scratch, lane);
+        if (q < nB) skp_phase_b<K4>(A, e, q, scratch, lane);
     }
 }
 
@@ -1013,8 +1015,13 @@ static int launch_skp(SkpArgs& A, cudaStream_t st)
     for (int e = 0; e < A.nbatch; e++) {
         const int b0 = e * A.T, b1 = std::min(A.Bl, b0 + A.T);
         const int64_t nA = ((int64_t)(b1 - b0) * A.n + SKP_ITEM - 1) / SKP_ITEM;
-        sketch_phase_kernel<0><<<(unsigned)ceil_div(nA, 8), 256, smem, st>>>(A, e);
-        sketch_phase_kernel<1><<<(unsigned)ceil_div(nB, 8), 256, smem, st>>>(A, e);
+        if (A.ld == 40) {  // k = r + 8 for the default rank 32
+            sketch_phase_kernel<0, 10><<<(unsigned)ceil_div(nA, 8), 256, smem, st>>>(A, e);
+            sketch_phase_kernel<1, 10><<<(unsigned)ceil_div(nB, 8), 256, smem, st>>>(A, e);
+        } else {
+            sketch_phase_kernel<0, 0><<<(unsigned)ceil_div(nA, 8), 256, smem, st>>>(A, e);
+            sketch_phase_kernel<1, 0><<<(unsigned)ceil_div(nB, 8), 256, smem, st>>>(A, e);
+        }
     }
     return check_launch("sketch_pass");
 }
