@@ -171,24 +171,19 @@ __device__ void spass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows, c
             out[t * 64 + fc * 8 + 2 * fr + 1] = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
         }
         __syncthreads();
-        // t_a (a < r) and su (a = r): thread (a, g) sums rows g, g + G, ...
-        const int G = (int)blockDim.x / 32;
-        double* red = s.scr;  // G x 32 partials
-        for (int a0 = 0; a0 <= r; a0 += 32) {
-            const int a = a0 + lane, g = warp;
+        // t_a (a < r) and su (a = r): one warp per column, lanes over rows
+        for (int a = warp; a <= r; a += nw) {
             double acc = 0.0;
-            if (a <= r)
-                for (int64_t i = g; i < rows; i += G) acc += x[i] * (a < r ? s.q64[i * ldq + a] : 1.0);
-            red[g * 32 + lane] = acc;
-            __syncthreads();
-            if (g == 0 && a <= r) {
-                double v = 0.0;
-                for (int q = 0; q < G; q++) v += red[q * 32 + lane];
+            if (a < r)
+                for (int i = lane; i < rows; i += 32) acc += x[i] * s.q64[i * ldq + a];
+            else
+                for (int i = lane; i < rows; i += 32) acc += x[i];
+            acc = warp_sum(acc);
+            if (lane == 0) {
                 const int ta = a >> 3, tb = r >> 3;
                 const int t = ta * A.TP - ta * (ta - 1) / 2 + (tb - ta);
-                out[t * 64 + (a & 7) * 8 + (r & 7)] = v;
+                out[t * 64 + (a & 7) * 8 + (r & 7)] = acc;
             }
-            __syncthreads();
         }
         return;
     }
