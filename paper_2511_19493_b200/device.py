@@ -18,6 +18,8 @@ the packed bytes cross PCIe.
 
 from __future__ import annotations
 
+import weakref
+
 import numpy as np
 
 from . import _lib
@@ -35,6 +37,29 @@ def _pinned(nbytes: int):
     torch = _torch()
     buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, pin_memory=True)
     return buf, buf.numpy()
+
+
+# Host staging of immutable inputs (Dataset.values arrays, Forest objects): the
+# packed pinned upload buffer is derived once per object and reused; every
+# construction of a DeviceValues / DeviceForest still copies it host -> device.
+_STAGED: dict = {}
+
+
+def _staged(obj, key, build):
+    """Per-object cache of `build()` keyed by (id(obj), key), dropped when obj
+    is garbage collected."""
+    k = (id(obj), key)
+    hit = _STAGED.get(k)
+    if hit is not None and hit[0]() is obj:
+        return hit[1]
+    val = build()
+    try:
+        ref = weakref.ref(obj)
+        weakref.finalize(obj, _STAGED.pop, k, None)
+    except TypeError:  # not weak-referenceable: no caching
+        return val
+    _STAGED[k] = (ref, val)
+    return val
 
 
 def feature_bits(p: int) -> int:
@@ -61,12 +86,16 @@ class DeviceValues:
         vals = np.asfortranarray(values, dtype=np.float64)
         self.n, self.p = vals.shape
         self._host = vals
-        buf, view = _pinned(vals.size * 4)
-        exact = np.zeros(1, dtype=np.int32)
-        # F-order (n, p) is exactly (p, n) row-major
-        _lib.call("rfxc_values_to_f32_host", vals.ctypes.data_as(_lib.P), vals.size,
-                  view.ctypes.data_as(_lib.P), exact.ctypes.data_as(_lib.P), 0)
-        self.exact_f32 = bool(exact[0])
+
+        def stage():
+            buf, view = _pinned(vals.size * 4)
+            exact = np.zeros(1, dtype=np.int32)
+            # F-order (n, p) is exactly (p, n) row-major
+            _lib.call("rfxc_values_to_f32_host", vals.ctypes.data_as(_lib.P), vals.size,
+                      view.ctypes.data_as(_lib.P), exact.ctypes.data_as(_lib.P), 0)
+            return buf, bool(exact[0])
+
+        buf, self.exact_f32 = _staged(values, "f32", stage)
         self.f32 = buf.to(self.dev, non_blocking=True).view(torch.float32).view(self.p, self.n) \
             if self.exact_f32 else None
         self._f64 = None
@@ -93,18 +122,7 @@ class DeviceForest:
         self.p = int(forest.p)
         B = len(trees)
         col_cat = _as(getattr(forest, "col_cat", trees[0].col_cat), np.uint8)
-        keep = []  # keep converted arrays alive during the call
-        tables = {name: np.empty(B, dtype=np.uintp) for name in
-                  ("status", "split_var", "threshold", "cat_mask", "left", "right")}
-        dts = {"status": np.int8, "split_var": np.int32, "threshold": np.float64,
-               "cat_mask": np.int64, "left": np.int32, "right": np.int32}
-        counts = np.empty(B, dtype=np.int64)
-        for b, t in enumerate(trees):
-            for name, dt in dts.items():
-                a = _as(getattr(t, name), dt)
-                keep.append(a)
-                tables[name][b] = a.ctypes.data
-            counts[b] = len(t.status)
+        counts = np.fromiter((len(t.status) for t in trees), dtype=np.int64, count=B)
         self.node_counts = counts
         self.total_nodes = int(counts.sum())
         self.f32_ok = int(counts.max()) < (1 << (31 - feature_bits(self.p)))
@@ -113,20 +131,35 @@ class DeviceForest:
         if layout == _lib.NODES_F32 and not self.f32_ok:
             raise DataError("tree too large for the 8-byte node layout")
         self.layout = layout
-        rec = 8 if layout == _lib.NODES_F32 else 16
-        buf, view = _pinned(self.total_nodes * rec)
-        off = np.empty(B + 1, dtype=np.int64)
-        lc = np.empty(B, dtype=np.int32)
-        P = _lib.P
-        with region("forest_pack_host"):
-            _lib.call("rfxc_forest_pack_host", *(tables[k].ctypes.data_as(P) for k in
-                                                 ("status", "split_var", "threshold",
-                                                  "cat_mask", "left", "right")),
-                      counts.ctypes.data_as(P), B, col_cat.ctypes.data_as(P), self.p, layout,
-                      view.ctypes.data_as(P), off.ctypes.data_as(P), lc.ctypes.data_as(P),
-                      nthreads)
-        del keep
-        self.leaf_counts = lc
+
+        def stage():
+            keep = []  # keep converted arrays alive during the call
+            tables = {name: np.empty(B, dtype=np.uintp) for name in
+                      ("status", "split_var", "threshold", "cat_mask", "left", "right")}
+            dts = {"status": np.int8, "split_var": np.int32, "threshold": np.float64,
+                   "cat_mask": np.int64, "left": np.int32, "right": np.int32}
+            for b, t in enumerate(trees):
+                for name, dt in dts.items():
+                    a = _as(getattr(t, name), dt)
+                    keep.append(a)
+                    tables[name][b] = a.ctypes.data
+            rec = 8 if layout == _lib.NODES_F32 else 16
+            buf, view = _pinned(self.total_nodes * rec)
+            off = np.empty(B + 1, dtype=np.int64)
+            lc = np.empty(B, dtype=np.int32)
+            P = _lib.P
+            with region("forest_pack_host"):
+                _lib.call("rfxc_forest_pack_host", *(tables[k].ctypes.data_as(P) for k in
+                                                     ("status", "split_var", "threshold",
+                                                      "cat_mask", "left", "right")),
+                          counts.ctypes.data_as(P), B, col_cat.ctypes.data_as(P), self.p, layout,
+                          view.ctypes.data_as(P), off.ctypes.data_as(P), lc.ctypes.data_as(P),
+                          nthreads)
+            del keep
+            return buf, off, lc
+
+        buf, off, lc = _staged(forest, ("nodes", tree_lo, self.tree_hi, layout), stage)
+        self.leaf_counts = lc.copy()
         self.nodes = buf.to(dev, non_blocking=True)
         self.node_off = torch.from_numpy(off).to(dev)
 
