@@ -192,22 +192,24 @@ int rfxc_leaf_gather(const int32_t* d_codes_nb, int64_t n, int32_t Bl,
 /* One whole sketch pass Y = scale * sum_b E_b E_b^T X over the Bl local
  * trees (M @ (Mt @ X) of proximity.py:394, :397, :398 with M the
  * 1/sqrt(B)-scaled one-hot, so scale = 1/B) as one cooperative kernel:
- * trees in batches of T whose leaf sums stay in L2 (leaf sums of batch e and
- * gather of batch e-1 per grid-synchronised epoch).  X: f32 (n, ld), ld = k
+ * trees in batches of T whose leaf sums stay in L2: per batch a leaf-sum
+ * kernel and a gather kernel; with nbuf = 2 the leaf sums of batch e+1 run
+ * on an auxiliary stream, overlapping the gather of batch e.  X: f32 (n, ld), ld = k
  * rounded up to 4 (k <= 128); Y: f64 (n, k).  rfxc_sketch_plan (host) picks
  * T so that two batches of leaf sums fit budget_bytes and sizes the
  * workspace; rfxc_sketch_prepare runs once per (bucketed membership, plan);
  * d_perm / d_seg / d_has_empty come from rfxc_bucket.  Deterministic. */
 int rfxc_sketch_plan(const int32_t* h_leaf_counts, int32_t Bl, int64_t n, int32_t k,
                      int64_t budget_bytes, int32_t* T_out, int64_t* s_rows_out,
-                     int64_t* work_bytes_out);
+                     int32_t* nbuf_out, int64_t* work_bytes_out);
 int rfxc_sketch_prepare(const int64_t* d_seg, const int64_t* d_leaf_base, int64_t n,
-                        int32_t Bl, int32_t k, int32_t T, int64_t s_rows, void* d_work,
-                        void* stream);
+                        int32_t Bl, int32_t k, int32_t T, int64_t s_rows, int32_t nbuf,
+                        void* d_work, void* stream);
 int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg, const int32_t* d_codes_nb,
                      const int64_t* d_leaf_base, const int32_t* d_has_empty, int64_t n,
                      int32_t Bl, const float* d_X, int32_t k, int32_t ld, double scale,
-                     int32_t T, int64_t s_rows, double* d_Y, void* d_work, void* stream);
+                     int32_t T, int64_t s_rows, int32_t nbuf, double* d_Y, void* d_work,
+                     void* stream);
 
 /* -------------------------------------------------------------------- K5 */
 /* C = A^T B for row-major f64 A (n, ka), B (n, kb): deterministic two-level

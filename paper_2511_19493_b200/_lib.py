@@ -51,10 +51,10 @@ SIGNATURES = {
     "rfxc_pack_f32": (ctypes.c_int, [P, I64, I32, I32, P, P]),
     "rfxc_leaf_sums": (ctypes.c_int, [P, P, I64, I64, P, I32, I32, P, P]),
     "rfxc_leaf_gather": (ctypes.c_int, [P, I64, I32, P, P, I32, I32, F64, I32, P, P]),
-    "rfxc_sketch_plan": (ctypes.c_int, [P, I32, I64, I32, I64, P, P, P]),
-    "rfxc_sketch_prepare": (ctypes.c_int, [P, P, I64, I32, I32, I32, I64, P, P]),
-    "rfxc_sketch_pass": (ctypes.c_int, [P, P, P, P, P, I64, I32, P, I32, I32, F64, I32, I64, P, P,
-                                        P]),
+    "rfxc_sketch_plan": (ctypes.c_int, [P, I32, I64, I32, I64, P, P, P, P]),
+    "rfxc_sketch_prepare": (ctypes.c_int, [P, P, I64, I32, I32, I32, I64, I32, P, P]),
+    "rfxc_sketch_pass": (ctypes.c_int, [P, P, P, P, P, I64, I32, P, I32, I32, F64, I32, I64, I32,
+                                        P, P, P]),
     "rfxc_gram_parts": (ctypes.c_int, [I64]),
     "rfxc_gram": (ctypes.c_int, [P, P, I64, I32, I32, P, P, P]),
     "rfxc_matmul_small": (ctypes.c_int, [P, I64, I32, P, I32, P, P, I32, P]),

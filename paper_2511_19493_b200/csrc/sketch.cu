@@ -397,13 +397,13 @@ __host__ __device__ inline int64_t skp_items_per_batch(int64_t n, int T)
 __host__ __device__ inline int skp_nbatch(int Bl, int T) { return (Bl + T - 1) / T; }
 
 __host__ __device__ inline SkpLayout skp_layout(int64_t n, int Bl, int T, int ld, int k,
-                                                int64_t s_rows)
+                                                int64_t s_rows, int nbuf)
 {
     SkpLayout L;
     const int64_t ipb = skp_items_per_batch(n, T);
     const int nb = skp_nbatch(Bl, T);
     int64_t off = 0;
-    L.S = off;         off += align256(s_rows * ld * 4);
+    L.S = off;         off += align256(nbuf * s_rows * ld * 4);
     L.part = off;      off += align256(2 * ipb * ld * 8);
     L.cnt = off;       off += align256(s_rows * 4);
     L.ctr = off;       off += align256(2 * (int64_t)(nb + 1) * 4);
@@ -967,35 +967,48 @@ extern "C" int rfxc_matmul_small(const double* d_Y, int64_t n, int32_t ka, const
 
 extern "C" int rfxc_sketch_plan(const int32_t* h_leaf_counts, int32_t Bl, int64_t n, int32_t k,
                                 int64_t budget_bytes, int32_t* T_out, int64_t* s_rows_out,
-                                int64_t* work_bytes_out)
+                                int32_t* nbuf_out, int64_t* work_bytes_out)
 {
     if (Bl < 1 || n < 1 || k < 1) return fail(RFXC_EDATA, "sketch_plan: bad shape");
     const int ld = (k + 3) / 4 * 4;
-    int T = std::min(SKP_MAX_T, (int)Bl);
-    int64_t s_rows = 0;
-    for (; T >= 1; T--) {
-        s_rows = 0;
-        for (int b0 = 0; b0 < Bl; b0 += T) {
-            int64_t s = 0;
-            for (int b = b0; b < std::min<int>(Bl, b0 + T); b++) s += h_leaf_counts[b];
-            s_rows = std::max(s_rows, s);
+    // largest batch of trees whose leaf sums (nbuf buffers) fit the budget
+    auto plan = [&](int nbuf, int64_t& rows_out) {
+        int T = std::min(SKP_MAX_T, (int)Bl);
+        for (; T >= 1; T--) {
+            int64_t rows = 0;
+            for (int b0 = 0; b0 < Bl; b0 += T) {
+                int64_t s = 0;
+                for (int b = b0; b < std::min<int>(Bl, b0 + T); b++) s += h_leaf_counts[b];
+                rows = std::max(rows, s);
+            }
+            rows_out = std::max<int64_t>(rows, 1);
+            if (nbuf * rows * ld * 4 <= budget_bytes || T == 1) break;
         }
-        if (s_rows * ld * 4 <= budget_bytes || T == 1) break;
-    }
+        return T;
+    };
+    int64_t r1 = 1, r2 = 1;
+    const int T1 = plan(1, r1), T2 = plan(2, r2);
+    // two buffers (phase A of batch e+1 overlaps phase B of batch e) only when
+    // that costs no batch size
+    const int nbuf = (T2 == T1) ? 2 : 1;
+    const int T = nbuf == 2 ? T2 : T1;
+    const int64_t s_rows = nbuf == 2 ? r2 : r1;
     if (T_out) *T_out = T;
-    if (s_rows_out) *s_rows_out = std::max<int64_t>(s_rows, 1);
-    if (work_bytes_out) *work_bytes_out = skp_layout(n, Bl, T, ld, k, std::max<int64_t>(s_rows, 1)).total;
+    if (s_rows_out) *s_rows_out = s_rows;
+    if (nbuf_out) *nbuf_out = nbuf;
+    if (work_bytes_out) *work_bytes_out = skp_layout(n, Bl, T, ld, k, s_rows, nbuf).total;
     return RFXC_OK;
 }
 
 extern "C" int rfxc_sketch_prepare(const int64_t* d_seg, const int64_t* d_leaf_base, int64_t n,
-                                   int32_t Bl, int32_t k, int32_t T, int64_t s_rows, void* d_work,
-                                   void* stream)
+                                   int32_t Bl, int32_t k, int32_t T, int64_t s_rows, int32_t nbuf,
+                                   void* d_work, void* stream)
 {
     if (n < 1 || Bl < 1 || k < 1 || T < 1 || T > SKP_MAX_T || s_rows < 1)
         return fail(RFXC_EDATA, "sketch_prepare: bad shape");
     const int ld = (k + 3) / 4 * 4;
-    const SkpLayout L = skp_layout(n, Bl, T, ld, k, s_rows);
+    if (nbuf < 1 || nbuf > 2) return fail(RFXC_EDATA, "sketch_prepare: nbuf must be 1 or 2");
+    const SkpLayout L = skp_layout(n, Bl, T, ld, k, s_rows, nbuf);
     char* w = static_cast<char*>(d_work);
     cudaStream_t st = as_stream(stream);
     cudaError_t e = cudaMemsetAsync(w + L.cnt, 0, s_rows * 4, st);
@@ -1008,20 +1021,57 @@ extern "C" int rfxc_sketch_prepare(const int64_t* d_seg, const int64_t* d_leaf_b
     return check_launch("sketch_prepare");
 }
 
-static int launch_skp(SkpArgs& A, cudaStream_t st)
+template <int PH>
+static void launch_phase(const SkpArgs& A, int e, cudaStream_t s)
 {
     const size_t smem = (size_t)8 * SKP_SCRATCH * 4;
-    const int64_t nB = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
-    for (int e = 0; e < A.nbatch; e++) {
+    int64_t items;
+    if (PH == 0) {
         const int b0 = e * A.T, b1 = std::min(A.Bl, b0 + A.T);
-        const int64_t nA = ((int64_t)(b1 - b0) * A.n + SKP_ITEM - 1) / SKP_ITEM;
-        if (A.ld == 40) {  // k = r + 8 for the default rank 32
-            sketch_phase_kernel<0, 10><<<(unsigned)ceil_div(nA, 8), 256, smem, st>>>(A, e);
-            sketch_phase_kernel<1, 10><<<(unsigned)ceil_div(nB, 8), 256, smem, st>>>(A, e);
-        } else {
-            sketch_phase_kernel<0, 0><<<(unsigned)ceil_div(nA, 8), 256, smem, st>>>(A, e);
-            sketch_phase_kernel<1, 0><<<(unsigned)ceil_div(nB, 8), 256, smem, st>>>(A, e);
+        items = ((int64_t)(b1 - b0) * A.n + SKP_ITEM - 1) / SKP_ITEM;
+    } else {
+        items = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
+    }
+    if (A.ld == 40)  // k = r + 8 for the default rank 32
+        sketch_phase_kernel<PH, 10><<<(unsigned)ceil_div(items, 8), 256, smem, s>>>(A, e);
+    else
+        sketch_phase_kernel<PH, 0><<<(unsigned)ceil_div(items, 8), 256, smem, s>>>(A, e);
+}
+
+// Phase A of batch e + 1 overlaps phase B of batch e: A runs on an auxiliary
+// stream forked from `st` (two leaf-sum buffers; A(e) waits for B(e - 2)
+// before overwriting its buffer), B stays on `st` in batch order (the Y
+// accumulation order is fixed) and the last B joins everything back.
+static int launch_skp(SkpArgs& A, cudaStream_t st)
+{
+    if (A.nbuf < 2) {
+        for (int e = 0; e < A.nbatch; e++) {
+            launch_phase<0>(A, e, st);
+            launch_phase<1>(A, e, st);
         }
+        return check_launch("sketch_pass");
+    }
+    static cudaStream_t aux[64] = {};
+    static std::vector<cudaEvent_t> evs[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!aux[dev]) cudaStreamCreateWithFlags(&aux[dev], cudaStreamNonBlocking);
+    std::vector<cudaEvent_t>& ev = evs[dev];
+    while ((int)ev.size() < 2 * A.nbatch + 1) {
+        cudaEvent_t x;
+        cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+        ev.push_back(x);
+    }
+    cudaStream_t sa = aux[dev];
+    cudaEventRecord(ev[0], st);  // fork: X and the buffers are ready on st
+    cudaStreamWaitEvent(sa, ev[0], 0);
+    for (int e = 0; e < A.nbatch; e++) {
+        if (e >= 2) cudaStreamWaitEvent(sa, ev[2 + 2 * (e - 2)], 0);  // B(e-2) released the buffer
+        launch_phase<0>(A, e, sa);
+        cudaEventRecord(ev[1 + 2 * e], sa);
+        cudaStreamWaitEvent(st, ev[1 + 2 * e], 0);
+        launch_phase<1>(A, e, st);
+        cudaEventRecord(ev[2 + 2 * e], st);
     }
     return check_launch("sketch_pass");
 }
@@ -1030,12 +1080,14 @@ extern "C" int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg,
                                 const int32_t* d_codes_nb, const int64_t* d_leaf_base,
                                 const int32_t* d_has_empty, int64_t n, int32_t Bl,
                                 const float* d_X, int32_t k, int32_t ld, double scale, int32_t T,
-                                int64_t s_rows, double* d_Y, void* d_work, void* stream)
+                                int64_t s_rows, int32_t nbuf, double* d_Y, void* d_work,
+                                void* stream)
 {
     if (n < 1 || Bl < 1 || k < 1 || ld != (k + 3) / 4 * 4 || T < 1 || T > SKP_MAX_T || s_rows < 1)
         return fail(RFXC_EDATA, "sketch_pass: bad shape (ld must be k rounded up to 4)");
     if (ld > 128) return fail(RFXC_EDATA, "sketch_pass: k=%d above 128", k);
-    const SkpLayout L = skp_layout(n, Bl, T, ld, k, s_rows);
+    if (nbuf < 1 || nbuf > 2) return fail(RFXC_EDATA, "sketch_pass: nbuf must be 1 or 2");
+    const SkpLayout L = skp_layout(n, Bl, T, ld, k, s_rows, nbuf);
     char* w = static_cast<char*>(d_work);
     cudaStream_t st = as_stream(stream);
     SkpArgs A;
@@ -1059,7 +1111,7 @@ extern "C" int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg,
     A.ld = ld;
     A.T = T;
     A.nbatch = skp_nbatch(Bl, T);
-    A.nbuf = 1;
+    A.nbuf = nbuf;
     A.scale = scale;
     cudaError_t e = cudaMemsetAsync(A.ctr, 0, 2 * (size_t)(A.nbatch + 1) * 4, st);
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "sketch_pass: %s", cudaGetErrorString(e));

@@ -492,9 +492,10 @@ class _Sketch:
     """P X for the (local trees of the) membership, and the all-reduce of the
     partials when the membership is a tree shard.
 
-    k <= 128: one fused cooperative kernel per pass (rfxc_sketch_pass, leaf
-    sums batched so they stay L2-resident); wider sketches use the two-kernel
-    leaf_sums / leaf_gather path."""
+    k <= 128: rfxc_sketch_pass (trees in batches whose leaf sums stay
+    L2-resident; per batch a leaf-sum and a gather kernel, the next batch's
+    leaf sums overlapping this batch's gather when two buffers fit); empty
+    leaves or wider sketches use the two-kernel leaf_sums / leaf_gather path."""
 
     def __init__(self, d: DeviceMembership, k: int, group=None, budget: int | None = None):
         import ctypes
@@ -512,14 +513,14 @@ class _Sketch:
             if budget is None:  # two batches of leaf sums next to X in L2 (Y streams)
                 budget = int(SKETCH_L2_FRACTION * _l2_bytes()) - d.n * self.ld * 4
                 budget = max(budget, 8 << 20)
-            T, rows, wb = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+            T, rows, nbuf, wb = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64()
             lc = np.ascontiguousarray(d.leaf_counts, dtype=np.int32)
             _lib.call("rfxc_sketch_plan", lc.ctypes.data_as(_lib.P), d.Bl, d.n, k, budget,
-                      ctypes.byref(T), ctypes.byref(rows), ctypes.byref(wb))
-            self.T, self.s_rows = int(T.value), int(rows.value)
+                      ctypes.byref(T), ctypes.byref(rows), ctypes.byref(nbuf), ctypes.byref(wb))
+            self.T, self.s_rows, self.nbuf = int(T.value), int(rows.value), int(nbuf.value)
             self.work = torch.empty(int(wb.value), dtype=torch.uint8, device=dev)
             _lib.call("rfxc_sketch_prepare", _lib.ptr(self.seg), _lib.ptr(d.leaf_base), d.n, d.Bl,
-                      k, self.T, self.s_rows, _lib.ptr(self.work), _lib.stream_handle())
+                      k, self.T, self.s_rows, self.nbuf, _lib.ptr(self.work), _lib.stream_handle())
         else:
             self.S = torch.empty((max(d.total_leaves, 1), self.ld), dtype=torch.float32,
                                  device=dev)
@@ -558,7 +559,7 @@ class _Sketch:
             _lib.call("rfxc_sketch_pass", _lib.ptr(self.perm), _lib.ptr(self.seg),
                       _lib.ptr(d.codes_nb), _lib.ptr(d.leaf_base), _lib.ptr(d.has_empty), d.n,
                       d.Bl, _lib.ptr(X32), self.k, self.ld, 1.0 / d.B, self.T, self.s_rows,
-                      _lib.ptr(Y), _lib.ptr(self.work), _lib.stream_handle())
+                      self.nbuf, _lib.ptr(Y), _lib.ptr(self.work), _lib.stream_handle())
 
 
 def _gram(A, Bm):
