@@ -59,7 +59,8 @@ __host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return
 // d0/d1 = D[lane/4][2*(lane%4) + {0,1}].
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b)
 {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    // not volatile: a pure register op the compiler may schedule freely
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }

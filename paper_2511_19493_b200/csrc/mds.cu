@@ -45,7 +45,7 @@ constexpr int XS_SUM = 0, XS_DMAX = 1, XS_D = 2;
 constexpr int BS = 24;         // reduction-B slots
 constexpr int MAXRT = 24;      // r <= 192
 constexpr int SMS_MAXRP = 96;  // S kept in shared memory up to RP = 96
-constexpr int SMEM_BUDGET = 226 * 1024;
+constexpr int SMEM_BUDGET = 222 * 1024;  // + ~3 KB of static shared memory
 
 enum { QS_F64 = 0, QS_I8 = 1, QS_GLOBAL = 2 };
 
@@ -100,7 +100,6 @@ struct Sm {
     double* us;         // rows: v of this slice
     double* S;          // RP x RP mean-corrected S (zero padded)
     double* ts;         // PE: this matvec's reduction-A totals (staged)
-    double* scr;        // 32 x 32 scratch
     double* t;          // RP
     double* red;        // 32
     double* bc;         // BS broadcast slots
@@ -111,7 +110,7 @@ __host__ __device__ __forceinline__ int rp_of(int r) { return 8 * ((r + 7) / 8);
 // f64 slice row stride: >= RP (the zero-padded width) and = 4 (mod 16)
 // doubles, so the 4 rows of a DMMA fragment land on different bank groups
 __host__ __device__ __forceinline__ int ldq_of(int rp) { return rp + ((4 - rp % 16) + 16) % 16; }
-__host__ __device__ __forceinline__ int64_t pad16(int64_t x) { return (x + 15) / 16 * 16; }
+__host__ __device__ __forceinline__ int64_t pad16(int64_t x) { return (x + 31) / 32 * 32; }  // rows: 8 k-steps of 4
 
 // q'(row, c) of the local slice (c == r is the constant-one column)
 template <int QS>
@@ -159,16 +158,21 @@ __device__ void spass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows, c
             const double* pa = s.q64 + fr * ldq + 8 * ta + fc;
             const double* pb = s.q64 + fr * ldq + 8 * tb + fc;
             const double* px = x + fr;
-            double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-            for (int base = 0; base < rows16; base += 16) {
+            // eight independent accumulator chains over the 4-row k-steps
+            double d[8][2];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < 8; u++) d[u][0] = d[u][1] = 0.0;
+            for (int base = 0; base < rows16; base += 32) {
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
                     const int off = base + 4 * u;
                     dmma884(d[u][0], d[u][1], px[off] * pa[off * ldq], pb[off * ldq]);
                 }
             }
-            out[t * 64 + fc * 8 + 2 * fr] = (d[0][0] + d[1][0]) + (d[2][0] + d[3][0]);
-            out[t * 64 + fc * 8 + 2 * fr + 1] = (d[0][1] + d[1][1]) + (d[2][1] + d[3][1]);
+#pragma unroll
+            for (int j = 0; j < 2; j++)
+                out[t * 64 + fc * 8 + 2 * fr + j] = ((d[0][j] + d[1][j]) + (d[2][j] + d[3][j])) +
+                                                    ((d[4][j] + d[5][j]) + (d[6][j] + d[7][j]));
         }
         __syncthreads();
         // t_a (a < r) and su (a = r): one warp per column, lanes over rows
@@ -289,13 +293,14 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
 #pragma unroll 4
         for (int e = threadIdx.x; e < RP * RP; e += (int)blockDim.x) {
             const int a = e / RP, b = e % RP;
+            const int SL = RP + 4;  // padded row stride: 4 fragment rows on distinct banks
             double v = 0.0;
             if (a < r && b < r) {
                 const double g = tile_entry(A.cst, s.tab, TP, a, b);
                 v = tile_entry(T, s.tab, TP, a, b) - mean * g;
                 sgm += v * g;
             }
-            s.S[e] = v;
+            s.S[a * SL + b] = v;
         }
     } else {
         for (int e = threadIdx.x; e < r * r; e += (int)blockDim.x) {
@@ -337,19 +342,32 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
             // q^T S q over the upper-triangle tile pairs of the symmetric S:
             // Z = Q_(ta) S_(ta,tb) (2 k-steps), then ppu += w Z . Q_(tb)
             const double* pq = s.q64 + ia * s.ldq;
+            constexpr int NP = RT * (RT + 1) / 2;
+            double z[NP][2];
+            // all tile pairs' DMMAs first (independent accumulators), then the epilogue
 #pragma unroll
-            for (int ta = 0; ta < RT; ta++) {
+            for (int ks = 0; ks < 2; ks++) {
+                int pi = 0;
 #pragma unroll
-                for (int tb = ta; tb < RT; tb++) {
-                    double z0 = 0.0, z1 = 0.0;
+                for (int ta = 0; ta < RT; ta++) {
+                    const int kr = 8 * ta + 4 * ks + fr;
+                    const double a = pq[kr];
 #pragma unroll
-                    for (int ks = 0; ks < 2; ks++) {
-                        const int kr = 8 * ta + 4 * ks + fr;
-                        dmma884(z0, z1, pq[kr], s.S[kr * RP + 8 * tb + fc]);
+                    for (int tb = ta; tb < RT; tb++, pi++) {
+                        if (ks == 0) z[pi][0] = z[pi][1] = 0.0;
+                        dmma884(z[pi][0], z[pi][1], a, s.S[kr * (RP + 4) + 8 * tb + fc]);
                     }
-                    const double wgt = ta == tb ? 1.0 : 2.0;
-                    ppu += wgt * (z0 * pq[8 * tb + 2 * fr] + z1 * pq[8 * tb + 2 * fr + 1]);
                 }
+            }
+            {
+                int pi = 0;
+#pragma unroll
+                for (int ta = 0; ta < RT; ta++)
+#pragma unroll
+                    for (int tb = ta; tb < RT; tb++, pi++) {
+                        const double wgt = ta == tb ? 1.0 : 2.0;
+                        ppu += wgt * (z[pi][0] * pq[8 * tb + 2 * fr] + z[pi][1] * pq[8 * tb + 2 * fr + 1]);
+                    }
             }
 #pragma unroll
             for (int j = 0; j < 2 * RT; j++) pu += pq[4 * j + fr] * s.t[4 * j + fr];
@@ -362,7 +380,7 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
                 for (int tn = 0; tn < RT; tn++) {
                     double b;
                     if (SMS) {
-                        b = s.S[kr * RP + 8 * tn + fc];
+                        b = s.S[kr * (RP + 4) + 8 * tn + fc];
                     } else {
                         const int cb = 8 * tn + fc;
                         b = (kr < r && cb < r) ? tile_entry(T, s.tab, TP, kr, cb) -
@@ -439,11 +457,10 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     // shared memory: [S RPxRP if SMS] [t RP] [us rpb] [scales r] [codes rows x r]
     Sm s;
     s.S = reinterpret_cast<double*>(msm);
-    s.t = s.S + (SMS ? RP * RP : 0);
+    s.t = s.S + (SMS ? RP * (RP + 4) : 0);
     s.ts = s.t + RP;
     s.us = s.ts + (SMS ? A.PE : 0);
-    s.scr = s.us + pad16(A.rpb);
-    double* scs = s.scr + 32 * 32;
+    double* scs = s.us + pad16(A.rpb);
     s.sc = scs;
     s.q8 = reinterpret_cast<const int8_t*>(scs + r);
     s.ldq = ldq_of(RP);
@@ -733,7 +750,7 @@ static size_t plan_smem(MdsArgs& A)
     const bool sms = RP <= SMS_MAXRP;
     A.rpb = (A.n + grid_size() - 1) / grid_size();
     const size_t fixed =
-        ((sms ? (size_t)RP * RP + A.PE : 0) + RP + (size_t)pad16(A.rpb) + 32 * 32 + r) * 8;
+        ((sms ? (size_t)RP * (RP + 4) + A.PE : 0) + RP + (size_t)pad16(A.rpb) + r) * 8;
     const size_t f64 = (size_t)pad16(A.rpb) * ldq_of(RP) * 8;
     const size_t i8 = (size_t)A.rpb * r;
     if (fixed + f64 <= SMEM_BUDGET) {
