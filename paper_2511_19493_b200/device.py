@@ -62,6 +62,18 @@ def _staged(obj, key, build):
     return val
 
 
+UPLOAD_CHUNK_TREES = 128
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(dev):
+    torch = _torch()
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _COPY_STREAMS[key]
+
+
 def feature_bits(p: int) -> int:
     fb = 1
     while (1 << fb) < p:
@@ -96,8 +108,18 @@ class DeviceValues:
             return buf, bool(exact[0])
 
         buf, self.exact_f32 = _staged(values, "f32", stage)
-        self.f32 = buf.to(self.dev, non_blocking=True).view(torch.float32).view(self.p, self.n) \
-            if self.exact_f32 else None
+        self.ready = None
+        self.f32 = None
+        if self.exact_f32:  # on the copy stream; traverse() waits for `ready`
+            dst = torch.empty(vals.size * 4, dtype=torch.uint8, device=self.dev)
+            cs = _copy_stream(self.dev)
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                dst.copy_(buf, non_blocking=True)
+                self.ready = torch.cuda.Event()
+                self.ready.record(cs)
+            dst.record_stream(cs)
+            self.f32 = dst.view(torch.float32).view(self.p, self.n)
         self._f64 = None
 
     @property
@@ -160,8 +182,36 @@ class DeviceForest:
 
         buf, off, lc = _staged(forest, ("nodes", tree_lo, self.tree_hi, layout), stage)
         self.leaf_counts = lc.copy()
-        self.nodes = buf.to(dev, non_blocking=True)
+        self.node_off_host = off
         self.node_off = torch.from_numpy(off).to(dev)
+        rec = 8 if layout == _lib.NODES_F32 else 16
+        self._rec = rec
+        self._staging = buf
+        self._nodes = torch.empty(max(self.total_nodes * rec, 1), dtype=torch.uint8, device=dev)
+        # node records cross PCIe in tree chunks on a copy stream, so the
+        # traversal of chunk c overlaps the copy of chunk c + 1 (traverse())
+        self.chunks = []
+        step = UPLOAD_CHUNK_TREES
+        cs = _copy_stream(dev)
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            for c0 in range(0, B, step):
+                c1 = min(B, c0 + step)
+                a, b = int(off[c0]) * rec, int(off[c1]) * rec
+                self._nodes[a:b].copy_(buf[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                self.chunks.append((c0, c1, ev))
+        self._nodes.record_stream(cs)
+
+    @property
+    def nodes(self):
+        """The packed node records once every chunk has arrived (the current
+        stream waits for the copies)."""
+        torch = _torch()
+        for _c0, _c1, ev in self.chunks:
+            torch.cuda.current_stream().wait_event(ev)
+        return self._nodes
 
     @property
     def ntree(self) -> int:
@@ -274,10 +324,15 @@ def traverse(dforest: DeviceForest, dvalues: DeviceValues):
     n, Bl = dvalues.n, dforest.ntree
     dev = vals.device
     tm = torch.empty((Bl, n), dtype=torch.int32, device=dev)
+    cur = torch.cuda.current_stream()
+    if dvalues.ready is not None:
+        cur.wait_event(dvalues.ready)
     with region("leaf_codes"):
-        _lib.call("rfxc_leaf_codes", _lib.ptr(dforest.nodes), _lib.ptr(dforest.node_off),
-                  layout, dvalues.p, 0, Bl, _lib.ptr(vals), n, _lib.ptr(tm),
-                  _lib.stream_handle())
+        for c0, c1, ev in dforest.chunks:  # each chunk after its node records arrived
+            cur.wait_event(ev)
+            _lib.call("rfxc_leaf_codes", _lib.ptr(dforest._nodes), _lib.ptr(dforest.node_off),
+                      layout, dvalues.p, c0, c1, _lib.ptr(vals), n, _lib.ptr(tm[c0:c1]),
+                      _lib.stream_handle())
     nb = torch.empty((n, Bl), dtype=torch.int32, device=dev)
     _lib.call("rfxc_transpose_i32", _lib.ptr(tm), Bl, n, _lib.ptr(nb), _lib.stream_handle())
     return nb, tm, layout
