@@ -119,18 +119,20 @@ int rfxc_transpose_i32(const int32_t* d_in, int64_t rows, int64_t cols,
                        int32_t* d_out, void* stream);
 
 /* -------------------------------------------------------------------- K2 */
-/* Stable per-tree counting sort of samples by leaf (the bucket built inside
+/* Stable per-tree sort of samples by leaf (the counting sort inside
  * accumulate_pair_counts[_block], _kernels.py:458-468, :491-501), done once
- * and reused by K3/K4.  Inputs: codes_tm (Bl x n), leaf_base (Bl+1, int64,
- * exclusive prefix of leaf_counts).  Outputs: d_perm (Bl x n): samples of
- * tree b sorted by leaf, ascending within a leaf, the first member of every
- * leaf tagged with RFXC_PERM_FIRST; d_seg (leaf_base[Bl]+1): absolute start
- * of every leaf's run in d_perm (d_seg[last] = Bl*n); *d_has_empty = 1 when
- * some leaf has no member.  d_scratch: 4 * leaf_base[Bl] bytes (used only
- * for trees with too many leaves for shared memory). */
+ * and reused by K3/K4: LSD radix over 8-bit leaf digits, one CTA per tree.
+ * Inputs: codes_tm (Bl x n), leaf_base (Bl+1, int64, exclusive prefix of
+ * leaf_counts), max_leaf_count.  Outputs: d_perm (Bl x n): samples of tree b
+ * sorted by leaf, ascending within a leaf, the first member of every leaf
+ * tagged with RFXC_PERM_FIRST; d_seg (leaf_base[Bl]+1): absolute start of
+ * every leaf's run in d_perm (d_seg[last] = Bl*n; an empty leaf starts where
+ * the next one does); *d_has_empty = 1 when some leaf has no member.
+ * d_scratch: rfxc_bucket_scratch_bytes(n, Bl) bytes. */
+int64_t rfxc_bucket_scratch_bytes(int64_t n, int32_t Bl);
 int rfxc_bucket(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
                 const int64_t* d_leaf_base, int32_t max_leaf_count,
-                uint32_t* d_perm, int64_t* d_seg, int32_t* d_scratch,
+                uint32_t* d_perm, int64_t* d_seg, void* d_scratch,
                 int32_t* d_has_empty, void* stream);
 
 /* -------------------------------------------------------------------- K3 */

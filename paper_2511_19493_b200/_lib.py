@@ -41,6 +41,7 @@ SIGNATURES = {
     "rfxc_values_to_f32_host": (ctypes.c_int, [P, I64, P, P, I32]),
     "rfxc_leaf_codes": (ctypes.c_int, [P, P, I32, I32, I32, I32, P, I64, P, P]),
     "rfxc_transpose_i32": (ctypes.c_int, [P, I64, I64, P, P]),
+    "rfxc_bucket_scratch_bytes": (I64, [I64, I32]),
     "rfxc_bucket": (ctypes.c_int, [P, I64, I32, P, I32, P, P, P, P, P]),
     "rfxc_pair_counts": (ctypes.c_int, [P, I64, I32, I64, I64, I32, P, P]),
     "rfxc_triblock_count": (ctypes.c_int, [P, I64, I32, I64, I64, F64, P, P]),

@@ -282,7 +282,8 @@ class DeviceMembership:
             perm = torch.empty((self.Bl, self.n), dtype=torch.int32, device=dev)
             seg = torch.empty(self.total_leaves + 1, dtype=torch.int64, device=dev)
             maxl = int(self.leaf_counts.max())
-            scratch = torch.empty(max(self.total_leaves, 1), dtype=torch.int32, device=dev)
+            scratch = torch.empty(int(_lib.load().rfxc_bucket_scratch_bytes(self.n, self.Bl)),
+                                  dtype=torch.uint8, device=dev)
             has_empty = torch.empty(1, dtype=torch.int32, device=dev)
             with region("bucket"):
                 _lib.call("rfxc_bucket", _lib.ptr(self.codes_tm), self.n, self.Bl,

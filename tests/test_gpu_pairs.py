@@ -127,3 +127,54 @@ def test_bucket_is_stable_counting_sort(synth2k):
         lo, hi = d.leaf_base_host[b], d.leaf_base_host[b + 1]
         starts = seg[lo:hi + 1] - b * n
         assert np.array_equal(np.diff(starts), np.bincount(codes[:, b], minlength=hi - lo))
+
+
+def _bucket_case(codes, lc):
+    from paper_2511_19493_b200.device import DeviceMembership
+    d = DeviceMembership.from_host(codes, lc)
+    perm, seg = d.buckets()
+    return d, perm.cpu().numpy().view(np.uint32), seg.cpu().numpy()
+
+
+@pytest.mark.parametrize("n,L,mode", [
+    (1, 1, "dense"), (37, 3, "dense"), (4096, 200, "dense"), (4097, 256, "gaps"),
+    (5000, 257, "dense"), (9000, 700, "gaps"), (20000, 40000, "gaps"),
+    (70000, 70000, "sparse3"), (12000, 5000, "one_big"), (8193, 300, "tail_empty"),
+])
+def test_radix_bucket_edge_cases(built, n, L, mode):
+    """K2 on hand-built memberships: one, two and three 8-bit passes
+    (L <= 256, <= 65536, > 65536), partial tiles, leaves with no member at
+    the start / middle / end of the code range, one leaf holding most samples.
+    perm must be the stable argsort, RFXC_PERM_FIRST the leaf starts, seg the
+    run starts (empty leaf = start of the next one), has_empty exact."""
+    rng = np.random.default_rng(n + L)
+    B = 3
+    codes = np.empty((n, B), np.int32)
+    for b in range(B):
+        if mode == "dense":
+            c = rng.integers(0, L, n)
+            c[: min(n, L)] = np.arange(min(n, L))
+        elif mode == "gaps":
+            c = rng.integers(0, L, n) // 3 * 3 + (L > 3) * 1
+            c = np.minimum(c, L - 1)
+        elif mode == "sparse3":
+            c = rng.integers(L - 300, L, n)
+        elif mode == "one_big":
+            c = np.where(rng.random(n) < 0.9, L // 2, rng.integers(0, L, n))
+        else:  # tail_empty
+            c = rng.integers(0, L - 40, n)
+        codes[:, b] = c
+    lc = np.full(B, L, np.int32)
+    d, perm, seg = _bucket_case(codes, lc)
+    any_empty = False
+    for b in range(B):
+        want = np.argsort(codes[:, b], kind="stable")
+        assert np.array_equal(perm[b] & 0x7FFFFFFF, want)
+        sc = codes[want, b]
+        assert np.array_equal((perm[b] >> 31).astype(bool), np.r_[True, sc[1:] != sc[:-1]])
+        cnt = np.bincount(codes[:, b], minlength=L)
+        starts = seg[b * L:(b + 1) * L + 1] - b * n
+        assert starts[0] == 0 and np.array_equal(np.diff(starts), cnt)
+        any_empty |= bool((cnt == 0).any())
+    assert seg[-1] == B * n
+    assert bool(int(d.has_empty.item())) == any_empty
