@@ -378,7 +378,6 @@ matmul_small_kernel(const double* __restrict__ Y, int64_t n, int ka, const doubl
 // b0+t (one coalesced row segment of the (n, B) membership), then the T
 // leaf-sum rows are gathered as float4 lanes with f64 accumulation and
 // added to Y (scaled by 1/B in the last batch).
-constexpr int SKP_ITEM = 384;     // positions per phase-A item (12 sub-chunks of 32)
 constexpr int SKP_SAMPLES = 24;  // samples per phase-B item
 constexpr int SKP_RMAX = 4;      // row slots per warp (lane groups of k4 lanes)
 constexpr int SKP_MAX_T = 32;
@@ -389,18 +388,18 @@ struct SkpLayout {
 
 __host__ __device__ inline int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
 
-__host__ __device__ inline int64_t skp_items_per_batch(int64_t n, int T)
+__host__ __device__ inline int64_t skp_items_per_batch(int64_t n, int T, int64_t item)
 {
-    return (T * n + SKP_ITEM - 1) / SKP_ITEM;
+    return (T * n + item - 1) / item;
 }
 
 __host__ __device__ inline int skp_nbatch(int Bl, int T) { return (Bl + T - 1) / T; }
 
 __host__ __device__ inline SkpLayout skp_layout(int64_t n, int Bl, int T, int ld, int k,
-                                                int64_t s_rows, int nbuf)
+                                                int64_t s_rows, int nbuf, int64_t item)
 {
     SkpLayout L;
-    const int64_t ipb = skp_items_per_batch(n, T);
+    const int64_t ipb = skp_items_per_batch(n, T, item);
     const int nb = skp_nbatch(Bl, T);
     int64_t off = 0;
     L.S = off;         off += align256(nbuf * s_rows * ld * 4);
@@ -425,7 +424,7 @@ struct SkpArgs {
     int32_t* cnt;              // s_rows
     unsigned* ctr;             // 2 x (nbatch + 1)
     const int32_t* item_leaf;  // nbatch x ipb
-    int64_t n, s_rows, ipb;
+    int64_t n, s_rows, ipb, item;
     int Bl, k, ld, T, nbatch;
     int nbuf;                  // leaf-sum buffers (1: A(e), B(e) on one stream)
     double scale;
@@ -436,7 +435,7 @@ struct SkpArgs {
 // it of batch e (last g with seg[g] <= P < seg[g + 1]).
 __global__ void skp_item_leaf_kernel(const int64_t* __restrict__ seg,
                                      const int64_t* __restrict__ leaf_base, int64_t n, int Bl,
-                                     int T, int64_t ipb, int32_t* __restrict__ item_leaf)
+                                     int T, int64_t ipb, int64_t item, int32_t* __restrict__ item_leaf)
 {
     const int nb = skp_nbatch(Bl, T);
     const int64_t total = nb * ipb;
@@ -445,7 +444,7 @@ __global__ void skp_item_leaf_kernel(const int64_t* __restrict__ seg,
         const int e = (int)(q / ipb);
         const int64_t it = q % ipb;
         const int b0 = e * T, b1 = min(Bl, b0 + T);
-        const int64_t P = (int64_t)b0 * n + it * SKP_ITEM;
+        const int64_t P = (int64_t)b0 * n + it * item;
         if (P >= (int64_t)b1 * n) {
             item_leaf[q] = -1;
             continue;
@@ -474,6 +473,13 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // of the item cut at its start, 2 = last segment cut at its end, 3 = both
 // (the item lies inside the leaf).  Cut segments leave an f64 piece per item;
 // the last piece to arrive adds them in item order and writes the sum.
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int32_t* p, int v)
+{
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ void skp_emit(const SkpArgs& A, double a0, double a1, double a2,
                                          double a3, int64_t g, int kind, int64_t it, int64_t pos0,
                                          int64_t g0, float4* Sb, int lane, bool lead)
@@ -489,24 +495,25 @@ __device__ __forceinline__ void skp_emit(const SkpArgs& A, double a0, double a1,
     double* pp = A.part + (it * 2 + slot) * A.ld + 4 * lane;
     if (lead) {
 #pragma unroll
-        for (int q = 0; q < 4; q++) pp[q] = acc[q];
+        for (int q = 0; q < 4; q++) __stcg(pp + q, acc[q]);
     }
-    __threadfence();
+    // the warp barrier orders the lanes' piece stores before lane 0's release;
+    // the last arriver's acquire (and the barrier of the shuffle) orders the
+    // piece loads after every other item's release
     __syncwarp();
     int last = 0;
     if (lane == 0) {
         const int64_t s = A.seg[g], e = A.seg[g + 1];
-        const int npieces = (int)(((e - 1 - pos0) / SKP_ITEM) - ((s - pos0) / SKP_ITEM)) + 1;
-        const int old = atomicAdd(A.cnt + (g - g0), 1);
+        const int npieces = (int)(((e - 1 - pos0) / A.item) - ((s - pos0) / A.item)) + 1;
+        const int old = atom_add_acq_rel_gpu(A.cnt + (g - g0), 1);
         last = (old == npieces - 1);
         if (last) A.cnt[g - g0] = 0;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) return;
-    __threadfence();
     if (lead) {
         const int64_t s = A.seg[g], e = A.seg[g + 1];
-        const int64_t i0 = (s - pos0) / SKP_ITEM, i1 = (e - 1 - pos0) / SKP_ITEM;
+        const int64_t i0 = (s - pos0) / A.item, i1 = (e - 1 - pos0) / A.item;
         double t[4] = {0.0, 0.0, 0.0, 0.0};
         for (int64_t j = i0; j <= i1; j++) {
             const double* src = A.part + (j * 2 + (j == i0 ? 1 : 0)) * A.ld + 4 * lane;
@@ -566,7 +573,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
 {
     const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
     const int64_t pos0 = (int64_t)b0 * A.n, pend = (int64_t)b1 * A.n;
-    const int64_t P0 = pos0 + it * SKP_ITEM, P1 = min64(P0 + SKP_ITEM, pend);
+    const int64_t P0 = pos0 + it * A.item, P1 = min64(P0 + A.item, pend);
     const int g0 = (int)A.leaf_base[b0];
     float4* Sb = reinterpret_cast<float4*>(A.S + (int64_t)(e % A.nbuf) * A.s_rows * A.ld);
     const int k4 = K4 ? K4 : (A.ld >> 2);  // compile-time for the common widths
@@ -607,7 +614,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
         for (int j = 0; j < SKP_RMAX; j++) {
             mm[j] = (int)max64(0, min64(32, P1 - (P0 + 32 * (int64_t)(s0 + j))));
             fl[j] = __ballot_sync(0xffffffffu, lane < mm[j] && (pv[j] & RFXC_PERM_FIRST));
-            pbuf[j * 32 + lane] = pv[j] & ~RFXC_PERM_FIRST;
+            pbuf[j * 32 + lane] = (pv[j] & ~RFXC_PERM_FIRST) * (uint32_t)k4;  // row offset in float4
         }
         if (s0 == 0 && (fl[0] & 1u)) { ckind = 0; }  // the item starts a leaf
         __syncwarp();
@@ -626,28 +633,61 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
         int cur = gi + before + ((fs & 1u) && !first_sub ? 1 : 0);
         bool inside = (fs & 1u) != 0;  // current segment started inside this sub-chunk
         float4 acc = z4, head = z4;
-        const uint32_t* pb = pbuf + slot * 32;
-        for (int p0 = 0; p0 < 32; p0 += SKP_UA) {
-            float4 x[SKP_UA];
-#pragma unroll
-            for (int u = 0; u < SKP_UA; u++) {
-                const int p = p0 + u;
-                x[u] = (on && p < m) ? __ldg(X4 + (pb[p] * (uint32_t)k4 + c4)) : z4;
+        const uint32_t* pb = pbuf + (on ? slot : 0) * 32;  // idle lanes shadow slot 0
+        const char* xb = reinterpret_cast<const char*>(X4 + c4);
+        // leaf starts at p in (0, m)
+        const unsigned fsx = (fs & ~1u) & (m >= 32 ? 0xffffffffu : ((1u << m) - 1u));
+        auto flush = [&]() {
+            if (inside) {
+                if (on) Sb[(uint32_t)(cur - g0) * k4 + c4] = acc;
+            } else {
+                head = acc;
             }
-#pragma unroll
-            for (int u = 0; u < SKP_UA; u++) {
-                const int p = p0 + u;
-                if (p > 0 && p < m && ((fs >> p) & 1u)) {  // a leaf starts at p
-                    if (inside) {
-                        if (on) Sb[(uint32_t)(cur - g0) * k4 + c4] = acc;
-                    } else {
-                        head = acc;
-                    }
-                    cur++;
-                    inside = true;
-                    acc = z4;
+            cur++;
+            inside = true;
+            acc = z4;
+        };
+        static_assert(SKP_UA == 4, "index loads are uint4");
+        if (P1 - (P0 + 32 * (int64_t)s0) >= 32 * R) {
+            // every slot has 32 positions: no predicates (lanes past the last
+            // slot re-read slot 0's rows and never store)
+#pragma unroll 2
+            for (int p0 = 0; p0 < 32; p0 += 4) {
+                const uint4 ix = *reinterpret_cast<const uint4*>(pb + p0);
+                const float4 x0 = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.x << 4)));
+                const float4 x1 = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.y << 4)));
+                const float4 x2 = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.z << 4)));
+                const float4 x3 = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.w << 4)));
+                const unsigned f4 = (fsx >> p0) & 0xFu;
+                if (f4 == 0u) {
+                    f4add(acc, x0);
+                    f4add(acc, x1);
+                    f4add(acc, x2);
+                    f4add(acc, x3);
+                } else {
+                    if (f4 & 1u) flush();
+                    f4add(acc, x0);
+                    if (f4 & 2u) flush();
+                    f4add(acc, x1);
+                    if (f4 & 4u) flush();
+                    f4add(acc, x2);
+                    if (f4 & 8u) flush();
+                    f4add(acc, x3);
                 }
-                f4add(acc, x[u]);
+            }
+        } else {
+            for (int p0 = 0; p0 < 32; p0 += 4) {
+                const uint4 ix = *reinterpret_cast<const uint4*>(pb + p0);
+                const uint32_t ixs[4] = {ix.x, ix.y, ix.z, ix.w};
+                float4 x[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    x[u] = (on && p0 + u < m) ? __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ixs[u] << 4))) : z4;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    if ((fsx >> (p0 + u)) & 1u) flush();
+                    f4add(acc, x[u]);
+                }
             }
         }
         // join the slots' cut segments in position order (uniform over the warp)
@@ -784,7 +824,7 @@ __global__ void __launch_bounds__(256, PH == 0 ? SKP_MINB_A : 4) sketch_phase_ke
     const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (PH == 0) {
         const int b0 = e * A.T, b1 = min(A.Bl, b0 + A.T);
-        const int64_t nA = ((int64_t)(b1 - b0) * A.n + SKP_ITEM - 1) / SKP_ITEM;
+        const int64_t nA = ((int64_t)(b1 - b0) * A.n + A.item - 1) / A.item;
         if (q < nA) skp_phase_a<K4>(A, e, q, scratch, lane);
     } else {
         const int64_t nB = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
@@ -965,6 +1005,15 @@ extern "C" int rfxc_matmul_small(const double* d_Y, int64_t n, int32_t ka, const
     }
 }
 
+// Phase-A item (positions per warp): one item per resident phase-A warp of
+// a batch, a multiple of 32, at least one 3-slot step
+static int64_t skp_item_size(int64_t n, int T)
+{
+    const int64_t warps = (int64_t)sm_count() * SKP_MINB_A * 8;
+    const int64_t item = (T * n + warps - 1) / warps;
+    return std::max<int64_t>(96, (item + 31) / 32 * 32);
+}
+
 extern "C" int rfxc_sketch_plan(const int32_t* h_leaf_counts, int32_t Bl, int64_t n, int32_t k,
                                 int64_t budget_bytes, int32_t* T_out, int64_t* s_rows_out,
                                 int32_t* nbuf_out, int64_t* work_bytes_out)
@@ -996,7 +1045,7 @@ extern "C" int rfxc_sketch_plan(const int32_t* h_leaf_counts, int32_t Bl, int64_
     if (T_out) *T_out = T;
     if (s_rows_out) *s_rows_out = s_rows;
     if (nbuf_out) *nbuf_out = nbuf;
-    if (work_bytes_out) *work_bytes_out = skp_layout(n, Bl, T, ld, k, s_rows, nbuf).total;
+    if (work_bytes_out) *work_bytes_out = skp_layout(n, Bl, T, ld, k, s_rows, nbuf, skp_item_size(n, T)).total;
     return RFXC_OK;
 }
 
@@ -1008,15 +1057,16 @@ extern "C" int rfxc_sketch_prepare(const int64_t* d_seg, const int64_t* d_leaf_b
         return fail(RFXC_EDATA, "sketch_prepare: bad shape");
     const int ld = (k + 3) / 4 * 4;
     if (nbuf < 1 || nbuf > 2) return fail(RFXC_EDATA, "sketch_prepare: nbuf must be 1 or 2");
-    const SkpLayout L = skp_layout(n, Bl, T, ld, k, s_rows, nbuf);
+    const int64_t item = skp_item_size(n, T);
+    const SkpLayout L = skp_layout(n, Bl, T, ld, k, s_rows, nbuf, item);
     char* w = static_cast<char*>(d_work);
     cudaStream_t st = as_stream(stream);
     cudaError_t e = cudaMemsetAsync(w + L.cnt, 0, s_rows * 4, st);
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "sketch_prepare: %s", cudaGetErrorString(e));
-    const int64_t ipb = skp_items_per_batch(n, T);
+    const int64_t ipb = skp_items_per_batch(n, T, item);
     const int64_t total = skp_nbatch(Bl, T) * ipb;
     const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 8);
-    skp_item_leaf_kernel<<<grid, 256, 0, st>>>(d_seg, d_leaf_base, n, Bl, T, ipb,
+    skp_item_leaf_kernel<<<grid, 256, 0, st>>>(d_seg, d_leaf_base, n, Bl, T, ipb, item,
                                                reinterpret_cast<int32_t*>(w + L.item_leaf));
     return check_launch("sketch_prepare");
 }
@@ -1028,7 +1078,7 @@ static void launch_phase(const SkpArgs& A, int e, cudaStream_t s)
     int64_t items;
     if (PH == 0) {
         const int b0 = e * A.T, b1 = std::min(A.Bl, b0 + A.T);
-        items = ((int64_t)(b1 - b0) * A.n + SKP_ITEM - 1) / SKP_ITEM;
+        items = ((int64_t)(b1 - b0) * A.n + A.item - 1) / A.item;
     } else {
         items = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
     }
@@ -1087,7 +1137,8 @@ extern "C" int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg,
         return fail(RFXC_EDATA, "sketch_pass: bad shape (ld must be k rounded up to 4)");
     if (ld > 128) return fail(RFXC_EDATA, "sketch_pass: k=%d above 128", k);
     if (nbuf < 1 || nbuf > 2) return fail(RFXC_EDATA, "sketch_pass: nbuf must be 1 or 2");
-    const SkpLayout L = skp_layout(n, Bl, T, ld, k, s_rows, nbuf);
+    const int64_t item = skp_item_size(n, T);
+    const SkpLayout L = skp_layout(n, Bl, T, ld, k, s_rows, nbuf, item);
     char* w = static_cast<char*>(d_work);
     cudaStream_t st = as_stream(stream);
     SkpArgs A;
@@ -1105,7 +1156,8 @@ extern "C" int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg,
     A.item_leaf = reinterpret_cast<const int32_t*>(w + L.item_leaf);
     A.n = n;
     A.s_rows = s_rows;
-    A.ipb = skp_items_per_batch(n, T);
+    A.item = item;
+    A.ipb = skp_items_per_batch(n, T, item);
     A.Bl = Bl;
     A.k = k;
     A.ld = ld;
