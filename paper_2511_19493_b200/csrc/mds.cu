@@ -40,8 +40,8 @@ namespace cg = cooperative_groups;
 
 namespace rfxc {
 
-constexpr int XA = 16;         // extra reduction-A slots: sum v, dmax, d_f (f < 8)
-constexpr int XS_SUM = 0, XS_DMAX = 1, XS_D = 2;
+constexpr int XA = 16;         // extra reduction-A slots: sum v, dmax, d_f (f < 8), sum v c, sum v d
+constexpr int XS_SUM = 0, XS_DMAX = 1, XS_D = 2, XS_CI = 10, XS_DI = 11;
 constexpr int BS = 24;         // reduction-B slots
 constexpr int MAXRT = 24;      // r <= 192
 constexpr int SMS_MAXRP = 96;  // S kept in shared memory up to RP = 96
@@ -70,6 +70,11 @@ struct MdsArgs {
     double* sparts;         // grid x PE
     double* tot;            // PE
     double* cst;            // NT * 64: C' = sum q' q'^T
+    double* sc;             // RP x (RP + 4): mean-corrected S of the last reduction (zero padded)
+    double* tc;             // RP + 4: mean-corrected t; tc[RP] = su
+    double* ci;             // n: q_i^T C q_i (C = Q^T Q)
+    double* di;             // n: q_i . c (c = Q^T 1)
+    int RPs;                // RP of the instantiated kernel (sc stride RPs + 4)
     double* bparts;         // 2 x grid x BS
     double* coords;         // n x k
     double* info;           // k x 4
@@ -101,8 +106,9 @@ struct Sm {
     double* S;          // RP x RP mean-corrected S (zero padded)
     double* ts;         // PE: this matvec's reduction-A totals (staged)
     double* t;          // RP
-    double* red;        // 32
+    double* red;        // 16 x 32
     double* bc;         // BS broadcast slots
+    double* kc;         // 2 constants
     int* tab;           // NT x 2 tile coordinates
 };
 
@@ -139,6 +145,7 @@ __device__ __forceinline__ double qraw(const MdsArgs& A, const Sm& s, int64_t r0
 template <int QS>
 __device__ void spass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows, const double* x)
 {
+    (void)r0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int fr = lane & 3, fc = lane >> 2;
     const int r = A.r;
@@ -215,31 +222,149 @@ __device__ void spass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows, c
     }
 }
 
-// fixed-order block reduction of m per-thread values into out[0..m)
-__device__ void block_sums(double* v, int m, double* red, double* out)
+// S'(x) partial of this CTA for a smem-resident f64 slice with r <= 8 * RT
+// (RT <= 4): four warps split the 4-row k-steps and each accumulates the
+// whole upper triangle (one B fragment per column tile per k-step, the A
+// fragment is x times it, RT(RT+1)/2 DMMA chains) plus t = sum x q and
+// sum x; the four warp partials are added in warp order 3, 2, 1, 0 through
+// shared memory `buf` (>= 32 * (RT(RT+1) + RT + 1) doubles).
+constexpr int SP_W = 4;
+template <int RT>
+__device__ void spass4(const MdsArgs& A, const Sm& s, int64_t rows, const double* x, double* buf)
 {
-    for (int j = 0; j < m; j++) {
-        const double x = block_sum(v[j], red);
-        if (threadIdx.x == 0) out[j] = x;
+    constexpr int NP = RT * (RT + 1) / 2;
+    constexpr int NV = 2 * NP + RT + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane & 3, fc = lane >> 2;
+    const int r = A.r, ldq = s.ldq;
+    double* out = A.sparts + (int64_t)blockIdx.x * A.PE;
+    double v[NV];
+#pragma unroll
+    for (int j = 0; j < NV; j++) v[j] = 0.0;
+    if (warp < SP_W) {
+        const int nks = (int)(pad16(rows) >> 2);
+        const int k0 = warp * nks / SP_W, k1 = (warp + 1) * nks / SP_W;
+        const double* pq = s.q64 + fc;
+#pragma unroll 2
+        for (int ks = k0; ks < k1; ks++) {
+            const int i = 4 * ks + fr;
+            const double xq = x[i];
+            double b[RT], a[RT];
+#pragma unroll
+            for (int t = 0; t < RT; t++) {
+                b[t] = pq[i * ldq + 8 * t];
+                a[t] = xq * b[t];
+                v[2 * NP + t] += a[t];
+            }
+            v[2 * NP + RT] += xq;
+            int pi = 0;
+#pragma unroll
+            for (int ta = 0; ta < RT; ta++)
+#pragma unroll
+                for (int tb = ta; tb < RT; tb++, pi++) dmma884(v[2 * pi], v[2 * pi + 1], a[ta], b[tb]);
+        }
+        // t and sum x over the 4 row phases of the fragment
+#pragma unroll
+        for (int j = 2 * NP; j < NV; j++) {
+            v[j] += __shfl_xor_sync(0xffffffffu, v[j], 1);
+            v[j] += __shfl_xor_sync(0xffffffffu, v[j], 2);
+        }
+    }
+    for (int w = SP_W - 1; w >= 1; w--) {
+        if (warp == w) {
+#pragma unroll
+            for (int j = 0; j < NV; j++) buf[j * 32 + lane] = v[j];
+        }
+        __syncthreads();
+        if (warp == w - 1) {
+#pragma unroll
+            for (int j = 0; j < NV; j++) v[j] += buf[j * 32 + lane];
+        }
         __syncthreads();
     }
+    if (warp == 0) {
+        const int RTq = (r + 7) / 8;
+        int pi = 0;
+#pragma unroll
+        for (int ta = 0; ta < RT; ta++)
+#pragma unroll
+            for (int tb = ta; tb < RT; tb++, pi++) {
+                if (tb >= RTq) continue;
+                const int t = ta * A.TP - ta * (ta - 1) / 2 + (tb - ta);
+                out[t * 64 + fc * 8 + 2 * fr] = v[2 * pi];
+                out[t * 64 + fc * 8 + 2 * fr + 1] = v[2 * pi + 1];
+            }
+        if (fr == 0) {
+            const int tbr = r >> 3;
+#pragma unroll
+            for (int t = 0; t < RT; t++) {
+                const int a = 8 * t + fc;
+                if (a < r) {
+                    const int ta = a >> 3;
+                    out[(ta * A.TP - ta * (ta - 1) / 2 + (tbr - ta)) * 64 + (a & 7) * 8 + (r & 7)] = v[2 * NP + t];
+                }
+            }
+            if (fc == 0)
+                out[(tbr * A.TP - tbr * (tbr - 1) / 2) * 64 + (r & 7) * 8 + (r & 7)] = v[2 * NP + RT];
+        }
+    }
+}
+
+// fixed-order block reduction of m <= 16 per-thread values into out[0..m)
+// (warp trees, then the warp partials in warp order); red >= 16 * warps
+__device__ void block_sums(double* v, int m, double* red, double* out)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+#pragma unroll
+    for (int j = 0; j < 16; j++)
+        if (j < m) {
+            const double x = warp_sum(v[j]);
+            if (lane == 0) red[warp * 16 + j] = x;
+        }
+    __syncthreads();
+    if ((int)threadIdx.x < m) {
+        double t = 0.0;
+        for (int w = 0; w < nw; w++) t += red[w * 16 + threadIdx.x];
+        out[threadIdx.x] = t;
+    }
+    __syncthreads();
 }
 
 // Distributed final reduction of the grid's reduction-A partials into tot:
 // one warp per entry, lanes over blocks in order; the dmax slot takes a max.
-__device__ void final_a(const MdsArgs& A, int entries)
+__device__ void final_a(const MdsArgs& A, int entries, const int* tab)
 {
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * (int)(blockDim.x >> 5) + (threadIdx.x >> 5), nw = gridDim.x * (int)(blockDim.x >> 5);
     const int dm = A.NT * 64 + XS_DMAX;
+    const int r = A.r, SL = A.RPs + 4;
+    if (gw >= entries) return;
+    // mean(v) from the sum slot (same order as its own entry below)
+    double sv = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) sv += A.sparts[(int64_t)b * A.PE + A.NT * 64 + XS_SUM];
+    const double mean = warp_sum(sv) / (double)A.n;
     for (int e = gw; e < entries; e += nw) {
-        double v = (e == dm) ? 0.0 : 0.0;
+        double v = 0.0;
         for (int b = lane; b < (int)gridDim.x; b += 32) {
             const double x = A.sparts[(int64_t)b * A.PE + e];
             v = (e == dm) ? fmax(v, x) : v + x;
         }
         v = (e == dm) ? warp_max(v) : warp_sum(v);
-        if (lane == 0) A.tot[e] = v;
+        if (lane != 0) continue;
+        A.tot[e] = v;
+        if (e >= A.NT * 64 || !A.sc) continue;
+        // S'(v) entry -> mean-corrected S, t or su
+        const int t = e >> 6, ta = tab[2 * t], tb = tab[2 * t + 1];
+        const int a = 8 * ta + ((e >> 3) & 7), b = 8 * tb + (e & 7);
+        const double c = v - mean * A.cst[e];
+        if (a < r && b < r) {
+            A.sc[a * SL + b] = c;
+            if (ta != tb) A.sc[b * SL + a] = c;
+        } else if (a < r && b == r) {
+            A.tc[a] = c;
+        } else if (a == r && b == r) {
+            A.tc[A.RPs] = c;
+        }
     }
 }
 
@@ -282,47 +407,40 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
     // totals staged in shared memory (one coalesced pass), then the mean-
     // corrected S, t and the closed-form mean of z
     const double* T = A.tot;
-    if (SMS) {
-        for (int e = threadIdx.x; e < A.PE; e += (int)blockDim.x) s.ts[e] = A.tot[e];
+    const double mean = rmode == 3 ? 0.0 : T[A.NT * 64 + XS_SUM] / (double)n;
+    double ct = 0.0, sgm = 0.0, su = 0.0;
+    if (rmode == 3) {
+        // s.S / s.t hold C and c: the row pass gives c_i and d_i
+    } else if (SMS) {
+        // S, t and su were corrected by final_a; the two scalar sums follow
+        // from the per-row constants: sum_ab S_ab C_ab = sum_i v_i c_i - mean |C|^2
+        for (int e = threadIdx.x; e < RP * (RP + 4); e += (int)blockDim.x) s.S[e] = A.sc[e];
+        for (int a = threadIdx.x; a < RP; a += (int)blockDim.x) s.t[a] = A.tc[a];
+        su = A.tc[RP];
+        sgm = T[A.NT * 64 + XS_CI] - mean * s.kc[0];
+        ct = T[A.NT * 64 + XS_DI] - mean * s.kc[1];
         __syncthreads();
-        T = s.ts;
-    }
-    const double mean = T[A.NT * 64 + XS_SUM] / (double)n;
-    double ct = 0.0, sgm = 0.0;
-    if (SMS) {
-#pragma unroll 4
-        for (int e = threadIdx.x; e < RP * RP; e += (int)blockDim.x) {
-            const int a = e / RP, b = e % RP;
-            const int SL = RP + 4;  // padded row stride: 4 fragment rows on distinct banks
-            double v = 0.0;
-            if (a < r && b < r) {
-                const double g = tile_entry(A.cst, s.tab, TP, a, b);
-                v = tile_entry(T, s.tab, TP, a, b) - mean * g;
-                sgm += v * g;
-            }
-            s.S[a * SL + b] = v;
-        }
     } else {
         for (int e = threadIdx.x; e < r * r; e += (int)blockDim.x) {
             const int a = e / r, b = e % r;
             const double g = tile_entry(A.cst, s.tab, TP, a, b);
             sgm += (tile_entry(T, s.tab, TP, a, b) - mean * g) * g;
         }
-    }
-    for (int a = threadIdx.x; a < RP; a += (int)blockDim.x) {
-        double v = 0.0;
-        if (a < r) {
-            const double c = tile_entry(A.cst, s.tab, TP, a, r);
-            v = tile_entry(T, s.tab, TP, a, r) - mean * c;
-            ct += c * v;
+        for (int a = threadIdx.x; a < RP; a += (int)blockDim.x) {
+            double v = 0.0;
+            if (a < r) {
+                const double c = tile_entry(A.cst, s.tab, TP, a, r);
+                v = tile_entry(T, s.tab, TP, a, r) - mean * c;
+                ct += c * v;
+            }
+            s.t[a] = v;
         }
-        s.t[a] = v;
+        __syncthreads();
+        su = tile_entry(T, s.tab, TP, r, r) - mean * tile_entry(A.cst, s.tab, TP, r, r);
+        ct = block_sum(ct, s.red);
+        sgm = block_sum(sgm, s.red);
     }
-    __syncthreads();
-    const double su = tile_entry(T, s.tab, TP, r, r) - mean * tile_entry(A.cst, s.tab, TP, r, r);
     const double pm = A.pmax;
-    ct = block_sum(ct, s.red);
-    sgm = block_sum(sgm, s.red);
     const double mz = (pm * pm) * su - 2.0 * pm * ct / (double)n + sgm / (double)n;
     double dfl[8];
     for (int f = 0; f < nf; f++) dfl[f] = lam_s[f] * T[A.NT * 64 + XS_D + f];
@@ -404,6 +522,13 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
         ppu += __shfl_xor_sync(0xffffffffu, ppu, 2);
         pu += __shfl_xor_sync(0xffffffffu, pu, 1);
         pu += __shfl_xor_sync(0xffffffffu, pu, 2);
+        if (rmode == 3) {
+            if (va && fr == 0) {
+                A.ci[r0 + ia] = ppu;
+                A.di[r0 + ia] = pu;
+            }
+            continue;
+        }
         if (va && fr == 0) {
             const int64_t g = r0 + ia;
             const double zi = (pm * pm) * su - 2.0 * pm * pu + ppu;
@@ -443,8 +568,9 @@ template <int QS, int RT, int NTH>
 __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
 {
     extern __shared__ __align__(16) unsigned char msm[];
-    __shared__ double red[32];
+    __shared__ double red[16 * 32];
     __shared__ double bc[BS];
+    __shared__ double kc[2];  // sum_ab C_ab^2, sum_a c_a^2
     __shared__ double lam_s[8];
     __shared__ int tab[2 * 300];
     cg::grid_group grid = cg::this_grid();
@@ -459,7 +585,7 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     s.S = reinterpret_cast<double*>(msm);
     s.t = s.S + (SMS ? RP * (RP + 4) : 0);
     s.ts = s.t + RP;
-    s.us = s.ts + (SMS ? A.PE : 0);
+    s.us = s.ts;
     double* scs = s.us + pad16(A.rpb);
     s.sc = scs;
     s.q8 = reinterpret_cast<const int8_t*>(scs + r);
@@ -467,6 +593,7 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     s.q64 = scs + r;
     s.red = red;
     s.bc = bc;
+    s.kc = kc;
     s.tab = tab;
     if (threadIdx.x == 0) {
         int t = 0;
@@ -495,10 +622,14 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     int par = 0;
     const int EA = A.NT * 64 + XA;
 
+    auto sreduce = [&]() {
+        if constexpr (QS == QS_F64 && SMS && RT >= 2 && RT <= 4) spass4<RT>(A, s, rows, s.us, s.S);
+        else spass<QS>(A, s, r0, rows, s.us);
+    };
     // constants C' = sum q' q'^T (u = 1)
     for (int64_t i = threadIdx.x; i < rows; i += (int)blockDim.x) s.us[i] = 1.0;
     __syncthreads();
-    spass<QS>(A, s, r0, rows, s.us);
+    sreduce();
     grid.sync();
     {
         const int lane = threadIdx.x & 31;
@@ -509,32 +640,76 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
             v = warp_sum(v);
             if (lane == 0) A.cst[e] = v;
         }
+        // zero padding of the corrected S / t written by final_a
+        if (SMS) {
+            const int nsc = RP * (RP + 4);
+            for (int e = blockIdx.x * (int)blockDim.x + threadIdx.x; e < nsc + RP + 4;
+                 e += gridDim.x * (int)blockDim.x) {
+                if (e < nsc) A.sc[e] = 0.0;
+                else A.tc[e - nsc] = 0.0;
+            }
+        }
     }
     grid.sync();
+    if (SMS) {
+        // per-row constants c_i = q_i^T C q_i, d_i = q_i . c and |C|^2, |c|^2,
+        // with C = Q^T Q and c = Q^T 1 staged in s.S / s.t
+        const int SL = RP + 4;
+        double f2 = 0.0, n2 = 0.0;
+        for (int e = threadIdx.x; e < RP * SL; e += (int)blockDim.x) {
+            const int a = e / SL, b = e % SL;
+            double v = 0.0;
+            if (a < r && b < r) {
+                v = tile_entry(A.cst, s.tab, A.TP, a, b);
+                f2 += v * v;
+            }
+            s.S[e] = v;
+        }
+        for (int a = threadIdx.x; a < RP; a += (int)blockDim.x) {
+            const double v = a < r ? tile_entry(A.cst, s.tab, A.TP, a, r) : 0.0;
+            n2 += v * v;
+            s.t[a] = v;
+        }
+        f2 = block_sum(f2, s.red);
+        n2 = block_sum(n2, s.red);
+        if (threadIdx.x == 0) {
+            kc[0] = f2;
+            kc[1] = n2;
+        }
+        __syncthreads();
+        double dummy[BS];
+        rowpass<QS, RT>(A, s, r0, rows, 0, lam_s, 0, 3, 0.0, dummy);
+    }
 
     // reduction A of the slice's v (s.us) with nf deflation dots and the
     // previous update's max change; leaves the totals in A.tot
     unsigned long long t_last = gtime();
     auto reduce_a = [&](int nf, double dmax_local) {
         MDS_T(0);
-        spass<QS>(A, s, r0, rows, s.us);
+        sreduce();
         MDS_T(1);
-        double x[2 + 8];
-        for (int j = 0; j < 2 + nf; j++) x[j] = 0.0;
+        double x[XS_DI + 1];
+#pragma unroll
+        for (int j = 0; j <= XS_DI; j++) x[j] = 0.0;
         for (int64_t i = threadIdx.x; i < rows; i += (int)blockDim.x) {
             const double vi = s.us[i];
-            x[0] += vi;
-            for (int f = 0; f < nf; f++) x[2 + f] += A.V[(int64_t)f * n + r0 + i] * vi;
+            x[XS_SUM] += vi;
+#pragma unroll
+            for (int f = 0; f < 8; f++)
+                if (f < nf) x[XS_D + f] += A.V[(int64_t)f * n + r0 + i] * vi;
+            if (SMS) {
+                x[XS_CI] += A.ci[r0 + i] * vi;
+                x[XS_DI] += A.di[r0 + i] * vi;
+            }
         }
-        x[1] = 0.0;
         double* out = A.sparts + (int64_t)blockIdx.x * A.PE + A.NT * 64;
-        block_sums(x, 2 + nf, s.red, s.bc);
+        block_sums(x, XS_DI + 1, s.red, s.bc);
         const double dm = block_max(dmax_local, s.red);
-        if (threadIdx.x < 2 + nf) out[threadIdx.x] = threadIdx.x == XS_DMAX ? dm : s.bc[threadIdx.x];
+        if (threadIdx.x <= XS_DI) out[threadIdx.x] = threadIdx.x == XS_DMAX ? dm : s.bc[threadIdx.x];
         MDS_T(2);
         grid.sync();
         MDS_T(3);
-        final_a(A, EA);
+        final_a(A, EA, s.tab);
         MDS_T(4);
         grid.sync();
         MDS_T(5);
@@ -697,7 +872,7 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
 
 // ------------------------------------------------------------------- host
 struct Layout {
-    int64_t V, w, sparts, tot, cst, bparts, bytes;
+    int64_t V, w, sparts, tot, cst, bparts, sc, tc, ci, di, bytes;
 };
 
 static int grid_size() { return sm_count(); }
@@ -707,6 +882,18 @@ static void shape(MdsArgs& A)
     A.TP = (A.r + 1 + 7) / 8;
     A.NT = A.TP * (A.TP + 1) / 2;
     A.PE = A.NT * 64 + XA;
+}
+
+static int rt_inst(int r)
+{
+    const int rt = (r + 7) / 8;
+    if (rt <= 1) return 1;
+    if (rt <= 2) return 2;
+    if (rt <= 4) return 4;
+    if (rt <= 8) return 8;
+    if (rt <= 12) return 12;
+    if (rt <= 16) return 16;
+    return 24;
 }
 
 static Layout mds_layout(int64_t n, int r, int k)
@@ -728,21 +915,15 @@ static Layout mds_layout(int64_t n, int r, int k)
     L.tot = take(A.PE);
     L.cst = take((int64_t)A.NT * 64);
     L.bparts = take(2LL * G * BS);
+    const int RP = 8 * rt_inst(r);
+    L.sc = take((int64_t)RP * (RP + 4));
+    L.tc = take(RP + 4);
+    L.ci = take(n);
+    L.di = take(n);
     L.bytes = o;
     return L;
 }
 
-static int rt_inst(int r)
-{
-    const int rt = (r + 7) / 8;
-    if (rt <= 1) return 1;
-    if (rt <= 2) return 2;
-    if (rt <= 4) return 4;
-    if (rt <= 8) return 8;
-    if (rt <= 12) return 12;
-    if (rt <= 16) return 16;
-    return 24;
-}
 
 static size_t plan_smem(MdsArgs& A)
 {
@@ -750,7 +931,7 @@ static size_t plan_smem(MdsArgs& A)
     const bool sms = RP <= SMS_MAXRP;
     A.rpb = (A.n + grid_size() - 1) / grid_size();
     const size_t fixed =
-        ((sms ? (size_t)RP * (RP + 4) + A.PE : 0) + RP + (size_t)pad16(A.rpb) + r) * 8;
+        ((sms ? (size_t)RP * (RP + 4) : 0) + RP + (size_t)pad16(A.rpb) + r) * 8;
     const size_t f64 = (size_t)pad16(A.rpb) * ldq_of(RP) * 8;
     const size_t i8 = (size_t)A.rpb * r;
     if (fixed + f64 <= SMEM_BUDGET) {
@@ -817,6 +998,11 @@ static void bind(MdsArgs& A, const Layout& L, void* d_work)
     A.tot = reinterpret_cast<double*>(base + L.tot);
     A.cst = reinterpret_cast<double*>(base + L.cst);
     A.bparts = reinterpret_cast<double*>(base + L.bparts);
+    A.sc = reinterpret_cast<double*>(base + L.sc);
+    A.tc = reinterpret_cast<double*>(base + L.tc);
+    A.ci = reinterpret_cast<double*>(base + L.ci);
+    A.di = reinterpret_cast<double*>(base + L.di);
+    A.RPs = 8 * rt_inst(A.r);
 }
 
 }  // namespace rfxc

@@ -16,9 +16,13 @@ for it in its:
     cfg = M.PowerIterConfig(seed=0, max_iterations=it, tol=1e-30, k=1)
     M.mds_lowrank(lr, cfg)
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    e = M.mds_lowrank(lr, cfg)
-    b.record()
-    torch.cuda.synchronize()
-    print(f"n={n} r={r} iterations={it}: {a.elapsed_time(b):.3f} ms", flush=True)
+    ts = []
+    for rep in range(7):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        e = M.mds_lowrank(lr, cfg)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    print(f"n={n} r={r} iterations={it}: median {ts[3]:.3f} ms (min {ts[0]:.3f})", flush=True)
