@@ -473,6 +473,18 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // of the item cut at its start, 2 = last segment cut at its end, 3 = both
 // (the item lies inside the leaf).  Cut segments leave an f64 piece per item;
 // the last piece to arrive adds them in item order and writes the sum.
+// leaf of bucketed position P: the last g in [lo, hi) with seg[g] <= P (an
+// empty leaf shares its start with the next one, so it is never returned)
+__device__ __forceinline__ int skp_leaf_at(const int64_t* __restrict__ seg, int lo, int hi, int64_t P)
+{
+    while (hi - lo > 1) {
+        const int m = (lo + hi) >> 1;
+        if (__ldg(seg + m) <= P) lo = m;
+        else hi = m;
+    }
+    return lo;
+}
+
 __device__ __forceinline__ int atom_add_acq_rel_gpu(int32_t* p, int v)
 {
     int old;
@@ -567,7 +579,8 @@ constexpr int SKP_UB = 4;  // phase B row loads in flight per lane
 // segments cut by sub-chunk boundaries (head / tail partials of every slot)
 // are then joined in position order into one f64 carry held by every slot,
 // which is emitted when its leaf ends (a piece when cut by the item edge).
-// Leaf ids follow from the first-member flags (no empty leaves on this path).
+// Leaf ids follow from the first-member flags, or, when the bucketing saw an
+// empty leaf (device flag, uniform), from a search of the run starts.
 template <int K4>
 __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf, int lane)
 {
@@ -588,6 +601,8 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
     if (lane == 0 && P1 < pend) tail_first = (__ldg(A.perm + P1) & RFXC_PERM_FIRST) != 0;
     const bool tail_open = !__shfl_sync(0xffffffffu, tail_first, 0);
     const int gi = A.item_leaf[(int64_t)e * A.ipb + it];
+    const int gN = (int)A.leaf_base[b1];
+    const bool he = *A.has_empty != 0;
 
     // carry: the open segment at the current position (f64, every lane holds
     // its column group), its leaf, whether it was cut at the item start and
@@ -630,20 +645,23 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
             if (j < slot) before += __popc(fj);
         }
         const bool first_sub = (s0 == 0 && slot == 0);
-        int cur = gi + before + ((fs & 1u) && !first_sub ? 1 : 0);
+        // leaf of this slot's first position (first-member flags count leaves
+        // unless some leaf is empty; then the run starts are searched)
+        const int64_t q0 = P0 + 32 * (int64_t)(s0 + slot);
+        int cur = he ? skp_leaf_at(A.seg, g0, gN, q0) : gi + before + ((fs & 1u) && !first_sub ? 1 : 0);
         bool inside = (fs & 1u) != 0;  // current segment started inside this sub-chunk
         float4 acc = z4, head = z4;
         const uint32_t* pb = pbuf + (on ? slot : 0) * 32;  // idle lanes shadow slot 0
         const char* xb = reinterpret_cast<const char*>(X4 + c4);
         // leaf starts at p in (0, m)
         const unsigned fsx = (fs & ~1u) & (m >= 32 ? 0xffffffffu : ((1u << m) - 1u));
-        auto flush = [&]() {
+        auto flush = [&](int p) {
             if (inside) {
                 if (on) Sb[(uint32_t)(cur - g0) * k4 + c4] = acc;
             } else {
                 head = acc;
             }
-            cur++;
+            cur = he ? skp_leaf_at(A.seg, g0, gN, q0 + p) : cur + 1;
             inside = true;
             acc = z4;
         };
@@ -665,13 +683,13 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
                     f4add(acc, x2);
                     f4add(acc, x3);
                 } else {
-                    if (f4 & 1u) flush();
+                    if (f4 & 1u) flush(p0);
                     f4add(acc, x0);
-                    if (f4 & 2u) flush();
+                    if (f4 & 2u) flush(p0 + 1);
                     f4add(acc, x1);
-                    if (f4 & 4u) flush();
+                    if (f4 & 4u) flush(p0 + 2);
                     f4add(acc, x2);
-                    if (f4 & 8u) flush();
+                    if (f4 & 8u) flush(p0 + 3);
                     f4add(acc, x3);
                 }
             }
@@ -685,7 +703,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
                     x[u] = (on && p0 + u < m) ? __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ixs[u] << 4))) : z4;
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    if ((fsx >> (p0 + u)) & 1u) flush();
+                    if ((fsx >> (p0 + u)) & 1u) flush(p0 + u);
                     f4add(acc, x[u]);
                 }
             }

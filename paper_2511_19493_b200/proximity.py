@@ -494,8 +494,8 @@ class _Sketch:
 
     k <= 128: rfxc_sketch_pass (trees in batches whose leaf sums stay
     L2-resident; per batch a leaf-sum and a gather kernel, the next batch's
-    leaf sums overlapping this batch's gather when two buffers fit); empty
-    leaves or wider sketches use the two-kernel leaf_sums / leaf_gather path."""
+    leaf sums overlapping this batch's gather when two buffers fit); wider
+    sketches use the two-kernel leaf_sums / leaf_gather path."""
 
     def __init__(self, d: DeviceMembership, k: int, group=None, budget: int | None = None):
         import ctypes
@@ -506,9 +506,9 @@ class _Sketch:
         self.perm, self.seg = d.buckets()
         dev = d.codes_nb.device
         self.group = group
-        # the fused pass derives leaf ids from first-member flags, which needs
-        # every leaf non-empty (always true for a forest's own training set)
-        self.fused = self.ld <= SKETCH_FUSED_MAX_LD and not int(d.has_empty.item())
+        # empty leaves are handled on the device (run-start search), so the
+        # choice needs no host read of the bucketing's flag
+        self.fused = self.ld <= SKETCH_FUSED_MAX_LD
         if self.fused:
             if budget is None:  # two batches of leaf sums next to X in L2 (Y streams)
                 budget = int(SKETCH_L2_FRACTION * _l2_bytes()) - d.n * self.ld * 4

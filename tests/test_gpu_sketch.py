@@ -82,7 +82,11 @@ def test_empty_leaves(orc):
     codes = (rng.integers(0, 40, size=(n, B)) * 3).astype(np.int32)  # only multiples of 3
     lc = np.full(B, 130, np.int32)
     sk, _ = check(orc, codes, lc, 12)
-    assert not sk.fused  # empty leaves take the two-kernel path
+    assert sk.fused  # leaf ids from a run-start search when a leaf is empty
+    check(orc, codes, lc, 40, budget=1)  # small batches, pieces across items
+    _, a = device_sketch(codes, lc, np.random.default_rng(1).normal(size=(n, 12)))
+    _, b = device_sketch(codes, lc, np.random.default_rng(1).normal(size=(n, 12)), fused=False)
+    np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-7 * np.abs(b).max())
 
 
 def test_deterministic_and_close_to_two_kernel_path(orc):
