@@ -134,6 +134,14 @@ int rfxc_bucket(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
                 const int64_t* d_leaf_base, int32_t max_leaf_count,
                 uint32_t* d_perm, int64_t* d_seg, void* d_scratch,
                 int32_t* d_has_empty, void* stream);
+/* The same for trees [tree_lo, tree_hi) only (d_has_empty is not cleared;
+ * the caller zeroes it once), so tree chunks can be bucketed as soon as
+ * their codes exist.  d_scratch: rfxc_bucket_scratch_bytes(n, tree_hi -
+ * tree_lo) bytes, private to the call until it completes. */
+int rfxc_bucket_trees(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
+                      const int64_t* d_leaf_base, int32_t max_leaf_count,
+                      int32_t tree_lo, int32_t tree_hi, uint32_t* d_perm, int64_t* d_seg,
+                      void* d_scratch, int32_t* d_has_empty, void* stream);
 
 /* -------------------------------------------------------------------- K3 */
 /* Exact same-leaf co-occurrence counts for rows [row_lo, row_hi), j > i,

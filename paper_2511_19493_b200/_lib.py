@@ -43,6 +43,7 @@ SIGNATURES = {
     "rfxc_transpose_i32": (ctypes.c_int, [P, I64, I64, P, P]),
     "rfxc_bucket_scratch_bytes": (I64, [I64, I32]),
     "rfxc_bucket": (ctypes.c_int, [P, I64, I32, P, I32, P, P, P, P, P]),
+    "rfxc_bucket_trees": (ctypes.c_int, [P, I64, I32, P, I32, I32, I32, P, P, P, P, P]),
     "rfxc_pair_counts": (ctypes.c_int, [P, I64, I32, I64, I64, I32, P, P]),
     "rfxc_triblock_count": (ctypes.c_int, [P, I64, I32, I64, I64, F64, P, P]),
     "rfxc_triblock_emit": (ctypes.c_int, [P, I64, I32, I64, I64, F64, P, P, P, P, P, P, P,
@@ -110,7 +111,7 @@ def check(rc: int, what: str = "") -> None:
 # kernels launched per successful call (host-side count for bench.py's
 # gpu_launches; rfxc_gram / rfxc_mds_power add their data-dependent extras)
 LAUNCHES = {"rfxc_values_to_f32": 1, "rfxc_forest_pack": 1, "rfxc_leaf_codes": 1,
-            "rfxc_transpose_i32": 1, "rfxc_bucket": 1, "rfxc_pair_counts": 1,
+            "rfxc_transpose_i32": 1, "rfxc_bucket": 1, "rfxc_bucket_trees": 1, "rfxc_pair_counts": 1,
             "rfxc_triblock_count": 1, "rfxc_triblock_emit": 1, "rfxc_exclusive_scan_i64": 1,
             "rfxc_normals": 1, "rfxc_pack_f32": 1, "rfxc_leaf_sums": 1, "rfxc_leaf_gather": 1,
             "rfxc_sketch_prepare": 1, "rfxc_sketch_pass": 1, "rfxc_orth_map": 1,
@@ -126,6 +127,17 @@ def call(name: str, *args) -> None:
     launch_count += LAUNCHES.get(name, 0)
     if name == "rfxc_mds_power":
         launch_count += int(args[6])  # start-vector normals, one per component
+    elif name == "rfxc_sketch_pass":  # a leaf-sum and a gather kernel per tree batch
+        Bl, T = int(args[6]), int(args[11])
+        launch_count += 2 * ((Bl + T - 1) // T) - 1
+    elif name in ("rfxc_bucket", "rfxc_bucket_trees"):  # launches of <= 2 trees per SM
+        trees = int(args[2]) if name == "rfxc_bucket" else int(args[6]) - int(args[5])
+        launch_count += max(0, (trees + 2 * _sms() - 1) // (2 * _sms()) - 1)
+
+
+def _sms() -> int:
+    import torch
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
 
 def ptr(t) -> ctypes.c_void_p:

@@ -227,17 +227,16 @@ extern "C" int64_t rfxc_bucket_scratch_bytes(int64_t n, int32_t Bl)
     return chunk * 2 * n * 8;
 }
 
-extern "C" int rfxc_bucket(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
-                           const int64_t* d_leaf_base, int32_t max_leaf_count,
-                           uint32_t* d_perm, int64_t* d_seg, void* d_scratch,
-                           int32_t* d_has_empty, void* stream)
+extern "C" int rfxc_bucket_trees(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
+                                 const int64_t* d_leaf_base, int32_t max_leaf_count,
+                                 int32_t tree_lo, int32_t tree_hi, uint32_t* d_perm, int64_t* d_seg,
+                                 void* d_scratch, int32_t* d_has_empty, void* stream)
 {
     if (n < 1 || Bl < 1 || max_leaf_count < 1) return fail(RFXC_EDATA, "bucket: bad shape");
+    if (tree_lo < 0 || tree_hi > Bl || tree_lo > tree_hi) return fail(RFXC_EDATA, "bucket: bad tree range");
     if (n >= (int64_t)RFXC_PERM_FIRST) return fail(RFXC_EDATA, "bucket: n exceeds 2^31");
     if (!d_scratch) return fail(RFXC_EDATA, "bucket: scratch required");
     cudaStream_t st = as_stream(stream);
-    cudaError_t e = cudaMemsetAsync(d_has_empty, 0, sizeof(int32_t), st);
-    if (e != cudaSuccess) return fail(RFXC_ECUDA, "bucket memset: %s", cudaGetErrorString(e));
     int bits = 0;
     while (bits < 31 && ((int64_t)1 << bits) < max_leaf_count) bits++;
     const int npass = std::max(1, (bits + 7) / 8);
@@ -249,12 +248,24 @@ extern "C" int rfxc_bucket(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
     }
     const int64_t chunk = std::min<int64_t>(Bl, (int64_t)sm_count() * 2);
     uint2* tmp = static_cast<uint2*>(d_scratch);
-    for (int64_t t0 = 0; t0 < Bl; t0 += chunk) {
-        const int nb = (int)std::min<int64_t>(chunk, Bl - t0);
+    for (int64_t t0 = tree_lo; t0 < tree_hi; t0 += chunk) {
+        const int nb = (int)std::min<int64_t>(chunk, tree_hi - t0);
         radix_bucket_kernel<RB_W, RB_U, 2><<<nb, RB_W * 32, sizeof(RbSmem<RB_W, RB_U>), st>>>(
             d_codes_tm, n, d_leaf_base, (int)t0, Bl, npass, tmp, d_perm, d_seg, d_has_empty);
         const int rc = check_launch("bucket");
         if (rc) return rc;
     }
     return RFXC_OK;
+}
+
+extern "C" int rfxc_bucket(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
+                           const int64_t* d_leaf_base, int32_t max_leaf_count,
+                           uint32_t* d_perm, int64_t* d_seg, void* d_scratch,
+                           int32_t* d_has_empty, void* stream)
+{
+    if (n < 1 || Bl < 1 || max_leaf_count < 1) return fail(RFXC_EDATA, "bucket: bad shape");
+    cudaError_t e = cudaMemsetAsync(d_has_empty, 0, sizeof(int32_t), as_stream(stream));
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "bucket memset: %s", cudaGetErrorString(e));
+    return rfxc_bucket_trees(d_codes_tm, n, Bl, d_leaf_base, max_leaf_count, 0, Bl, d_perm, d_seg,
+                             d_scratch, d_has_empty, stream);
 }

@@ -250,8 +250,9 @@ class DeviceMembership:
     lazily built per-tree leaf buckets."""
 
     def __init__(self, codes_nb, codes_tm, leaf_counts: np.ndarray, tree_lo: int, tree_hi: int,
-                 B: int):
+                 B: int, chunks=None):
         torch = _torch()
+        self.chunks = chunks  # traversal chunks (local c0, c1, event) or None
         self.codes_nb = codes_nb
         self.codes_tm = codes_tm
         self.n = int(codes_nb.shape[0])
@@ -282,13 +283,17 @@ class DeviceMembership:
             perm = torch.empty((self.Bl, self.n), dtype=torch.int32, device=dev)
             seg = torch.empty(self.total_leaves + 1, dtype=torch.int64, device=dev)
             maxl = int(self.leaf_counts.max())
-            scratch = torch.empty(int(_lib.load().rfxc_bucket_scratch_bytes(self.n, self.Bl)),
+            has_empty = torch.zeros(1, dtype=torch.int32, device=dev)
+            lib = _lib.load()
+            # one call over all trees: bucketing per traversal chunk on side
+            # streams was measured no faster (the traversal fills every SM)
+            scratch = torch.empty(int(lib.rfxc_bucket_scratch_bytes(self.n, self.Bl)),
                                   dtype=torch.uint8, device=dev)
-            has_empty = torch.empty(1, dtype=torch.int32, device=dev)
             with region("bucket"):
-                _lib.call("rfxc_bucket", _lib.ptr(self.codes_tm), self.n, self.Bl,
-                          _lib.ptr(self.leaf_base), maxl, _lib.ptr(perm), _lib.ptr(seg),
-                          _lib.ptr(scratch), _lib.ptr(has_empty), _lib.stream_handle())
+                _lib.call("rfxc_bucket_trees", _lib.ptr(self.codes_tm), self.n, self.Bl,
+                          _lib.ptr(self.leaf_base), maxl, 0, self.Bl, _lib.ptr(perm),
+                          _lib.ptr(seg), _lib.ptr(scratch), _lib.ptr(has_empty),
+                          _lib.stream_handle())
             self._perm, self._seg, self._has_empty = perm, seg, has_empty
         return self._perm, self._seg
 
@@ -328,12 +333,16 @@ def traverse(dforest: DeviceForest, dvalues: DeviceValues):
     cur = torch.cuda.current_stream()
     if dvalues.ready is not None:
         cur.wait_event(dvalues.ready)
+    done = []  # (c0, c1, event after the chunk's codes): K2 starts per chunk
     with region("leaf_codes"):
         for c0, c1, ev in dforest.chunks:  # each chunk after its node records arrived
             cur.wait_event(ev)
             _lib.call("rfxc_leaf_codes", _lib.ptr(dforest._nodes), _lib.ptr(dforest.node_off),
                       layout, dvalues.p, c0, c1, _lib.ptr(vals), n, _lib.ptr(tm[c0:c1]),
                       _lib.stream_handle())
+            cev = torch.cuda.Event()
+            cev.record(cur)
+            done.append((c0, c1, cev))
     nb = torch.empty((n, Bl), dtype=torch.int32, device=dev)
     _lib.call("rfxc_transpose_i32", _lib.ptr(tm), Bl, n, _lib.ptr(nb), _lib.stream_handle())
-    return nb, tm, layout
+    return nb, tm, done

@@ -160,8 +160,8 @@ def leaf_membership(forest, dataset, trees: tuple | None = None) -> LeafMembersh
     dvals = DeviceValues(dataset.values)
     layout = None if dvals.exact_f32 else _lib.NODES_F64
     dforest = DeviceForest(forest, *local, layout=layout)
-    nb, tm, _ = traverse(dforest, dvals)
-    dev = DeviceMembership(nb, tm, dforest.leaf_counts, lo, hi, B)
+    nb, tm, chunks = traverse(dforest, dvals)
+    dev = DeviceMembership(nb, tm, dforest.leaf_counts, lo, hi, B, chunks)
     return LeafMembership(leaf_counts=dforest.leaf_counts, _dev=dev)
 
 

@@ -18,8 +18,8 @@ print(f"trained {B} trees in {time.time()-t0:.1f}s", flush=True)
 dv = DeviceValues(ds.values)
 df = DeviceForest(forest, 0, B)
 for rep in range(2):
-    nb, tm, _ = traverse(df, dv)
-    dm = DeviceMembership(nb, tm, df.leaf_counts, 0, B, B)
+    nb, tm, chunks = traverse(df, dv)
+    dm = DeviceMembership(nb, tm, df.leaf_counts, 0, B, B, chunks)
     sk = P._Sketch(dm, 40)
     if rep == 0:
         lc = dm.leaf_counts

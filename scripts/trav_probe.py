@@ -13,16 +13,16 @@ forest = train(ds, TrainConfig(ntree=500, iseed=1), trees=(0, B))
 dv = DeviceValues(ds.values)
 df = DeviceForest(forest, 0, B)
 for _ in range(3):
-    nb, tm, _ = traverse(df, dv)
-    DeviceMembership(nb, tm, df.leaf_counts, 0, B, B).buckets()
+    nb, tm, chunks = traverse(df, dv)
+    DeviceMembership(nb, tm, df.leaf_counts, 0, B, B, chunks).buckets()
 torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 ev[0].record()
 for _ in range(5):
-    nb, tm, _ = traverse(df, dv)
+    nb, tm, chunks = traverse(df, dv)
 ev[1].record()
 for _ in range(5):
-    DeviceMembership(nb, tm, df.leaf_counts, 0, B, B).buckets()
+    DeviceMembership(nb, tm, df.leaf_counts, 0, B, B, chunks).buckets()
 ev[2].record()
 torch.cuda.synchronize()
 print(f"traverse {ev[0].elapsed_time(ev[1]) / 5:.3f} ms  bucket {ev[1].elapsed_time(ev[2]) / 5:.3f} ms  "
