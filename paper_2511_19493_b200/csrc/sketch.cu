@@ -207,9 +207,13 @@ leaf_gather_kernel(const int32_t* __restrict__ codes, int64_t n, int Bl,
 // per entry then adds the per-CTA partials in block order.  Deterministic.
 constexpr int GRAM_THREADS = 256;
 
+// partial-sum slots a Gram launch may write (the staged kernel uses up to one
+// part per SM of >= 64 rows, the fallback up to two per SM of >= 256 rows)
 int gram_parts(int64_t n)
 {
-    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 2));
+    const int64_t staged = std::min<int64_t>(ceil_div(n, 64), (int64_t)sm_count());
+    const int64_t fallback = std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 2);
+    return (int)std::max<int64_t>(1, std::max(staged, fallback));
 }
 
 // TAM x TBM accumulator tiles (compile-time indices); runtime TA <= TAM, TB <= TBM
@@ -293,6 +297,172 @@ __global__ void gram_final_kernel(const double* __restrict__ parts, int nparts, 
     for (int q = lane; q < nparts; q += 32) s += parts[(int64_t)q * E + e];
     s = warp_sum(s);
     if (lane == 0) C[(a0 + e / kb) * ldc + c0 + e % kb] = s;
+}
+
+// Staged Gram (ka, kb <= 128): a CTA per SM streams its contiguous row range
+// through shared memory in 32-row chunks (cp.async, zero-filled past the
+// end, next chunk in flight while the current one is multiplied) and every
+// warp owns whole 8x8 output tiles (upper tiles only when A == B), so no
+// cross-warp reduction is needed; the CTA's tiles go to parts[blk] and
+// gram_final adds the parts in block order.  Deterministic.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+constexpr int GS_CH = 32;
+constexpr int GS_MAXST = 8;
+
+// wait until at most n (< GS_MAXST) cp.async groups of this thread are pending
+__device__ __forceinline__ void cp_async_wait_dyn(int n)
+{
+    switch (n) {
+        case 0: cp_async_wait<0>(); break;
+        case 1: cp_async_wait<1>(); break;
+        case 2: cp_async_wait<2>(); break;
+        case 3: cp_async_wait<3>(); break;
+        case 4: cp_async_wait<4>(); break;
+        case 5: cp_async_wait<5>(); break;
+        case 6: cp_async_wait<6>(); break;
+        default: cp_async_wait<7>(); break;
+    }
+}
+
+__device__ __forceinline__ void cp_async8z(void* smem, const void* gmem, bool ok)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = ok ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+
+__host__ __device__ inline int gs_ld(int cols) { return cols + ((4 - cols % 16) + 16) % 16; }
+
+constexpr int GS_THREADS = 512;
+
+template <int MT>
+__global__ void __launch_bounds__(GS_THREADS, 1)
+gram_stage_kernel(const double* __restrict__ A, const double* __restrict__ Bm, int64_t n, int ka,
+                  int kb, int sym, int64_t rpp, int nst, double* __restrict__ parts)
+{
+    extern __shared__ __align__(16) double gss[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane & 3, fc = lane >> 2;
+    const int TA = (ka + 7) / 8, TB = (kb + 7) / 8;
+    const int lsa = gs_ld(8 * TA), lsb = sym ? lsa : gs_ld(8 * TB);
+    const int per = GS_CH * (lsa + (sym ? 0 : lsb));
+    const int64_t r0 = blockIdx.x * rpp, r1 = min64(n, r0 + rpp);
+    const int NT = sym ? TA * (TA + 1) / 2 : TA * TB;
+    int ta[MT], tb[MT];
+#pragma unroll
+    for (int m = 0; m < MT; m++) {
+        int t = warp + (GS_THREADS / 32) * m, a = 0, b = -1;
+        if (t < NT) {
+            if (sym) {
+                while (t >= TA - a) { t -= TA - a; a++; }
+                b = a + t;
+            } else {
+                a = t / TB;
+                b = t % TB;
+            }
+        }
+        ta[m] = a;
+        tb[m] = b;
+    }
+    double acc[MT][2];
+#pragma unroll
+    for (int m = 0; m < MT; m++) acc[m][0] = acc[m][1] = 0.0;
+    // each thread copies a fixed column of every rstep-th row of a chunk
+    const int GA = 8 * TA, GB = 8 * TB;
+    const int ca = threadIdx.x % GA, ra0 = threadIdx.x / GA, rsa = (int)blockDim.x / GA;
+    const int cb = threadIdx.x % GB, rb0 = threadIdx.x / GB, rsb = (int)blockDim.x / GB;
+    auto stage = [&](int64_t c, int buf) {
+        double* sa = gss + buf * per;
+        if (ra0 < GS_CH)
+            for (int row = ra0; row < GS_CH; row += rsa) {
+                const int64_t g = c + row;
+                const bool ok = g < r1 && ca < ka;
+                cp_async8z(sa + row * lsa + ca, ok ? A + g * ka + ca : A, ok);
+            }
+        if (!sym && rb0 < GS_CH) {
+            double* sb = sa + GS_CH * lsa;
+            for (int row = rb0; row < GS_CH; row += rsb) {
+                const int64_t g = c + row;
+                const bool ok = g < r1 && cb < kb;
+                cp_async8z(sb + row * lsb + cb, ok ? Bm + g * kb + cb : Bm, ok);
+            }
+        }
+        cp_async_commit();
+    };
+    // nst-deep pipeline: chunks it+1 .. it+nst-1 in flight while chunk it is used
+    const int nch = (int)((r1 - r0 + GS_CH - 1) / GS_CH);
+    for (int j = 0; j < nst - 1; j++) {
+        if (j < nch) stage(r0 + (int64_t)j * GS_CH, j);
+        else cp_async_commit();
+    }
+    int bl = nst - 1, bu = 0;  // buffer to load into / to use
+    for (int it = 0; it < nch; it++) {
+        const int nx = it + nst - 1;
+        if (nx < nch) stage(r0 + (int64_t)nx * GS_CH, bl);
+        else cp_async_commit();
+        bl = bl + 1 == nst ? 0 : bl + 1;
+        cp_async_wait_dyn(nst - 1);
+        __syncthreads();
+        const double* sa = gss + bu * per;
+        const double* sb = sym ? sa : sa + GS_CH * lsa;
+        bu = bu + 1 == nst ? 0 : bu + 1;
+#pragma unroll
+        for (int ks = 0; ks < GS_CH / 4; ks++) {
+            const double* ra = sa + (4 * ks + fr) * lsa + fc;
+            const double* rb = sb + (4 * ks + fr) * lsb + fc;
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (tb[m] >= 0) dmma884(acc[m][0], acc[m][1], ra[8 * ta[m]], rb[8 * tb[m]]);
+        }
+        __syncthreads();
+    }
+    double* out = parts + (int64_t)blockIdx.x * ka * kb;
+#pragma unroll
+    for (int m = 0; m < MT; m++) {
+        if (tb[m] < 0) continue;
+        const int a = 8 * ta[m] + fc;
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+            const int b = 8 * tb[m] + 2 * fr + j;
+            if (a < ka && b < kb) {
+                out[a * kb + b] = acc[m][j];
+                if (sym && ta[m] != tb[m]) out[b * kb + a] = acc[m][j];
+            }
+        }
+    }
+}
+
+template <int MT>
+static int launch_gram_stage(const double* d_A, const double* d_B, int64_t n, int ka, int kb,
+                             double* d_partials, double* d_C, cudaStream_t st)
+{
+    const int sym = (d_A == d_B && ka == kb) ? 1 : 0;
+    const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 64), sm_count()));
+    const int64_t rpp = ceil_div(n, parts);
+    const int TA = (ka + 7) / 8, TB = (kb + 7) / 8;
+    const size_t per = (size_t)GS_CH * (gs_ld(8 * TA) + (sym ? 0 : gs_ld(8 * TB))) * 8;
+    const int nst = (int)std::max<size_t>(2, std::min<size_t>(GS_MAXST, (size_t)(200 * 1024) / per));
+    const size_t smem = per * nst;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gram_stage_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+    }
+    gram_stage_kernel<MT><<<parts, GS_THREADS, smem, st>>>(d_A, d_B, n, ka, kb, sym, rpp, nst, d_partials);
+    int rc = check_launch("gram_stage");
+    if (rc) return rc;
+    gram_final_kernel<<<(unsigned)ceil_div((int64_t)ka * kb * 32, 256), 256, 0, st>>>(
+        d_partials, parts, ka, kb, d_C, kb, 0, 0);
+    return check_launch("gram_final");
 }
 
 // --------------------------------------------------------- small matmul
@@ -459,14 +629,7 @@ __global__ void skp_item_leaf_kernel(const int64_t* __restrict__ seg,
     }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
-{
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 
 // Emit one finished (or cut) leaf segment held by the slot-0 lanes (lane c4
 // owns columns 4c4..4c4+3 in f64).  kind: 0 = whole leaf, 1 = first segment
@@ -942,6 +1105,16 @@ extern "C" int rfxc_gram(const double* d_A, const double* d_B, int64_t n, int32_
     if (n < 1 || ka < 1 || kb < 1) return fail(RFXC_EDATA, "gram: bad shape ka=%d kb=%d", ka, kb);
     cudaStream_t st = as_stream(stream);
     const int TA = (ka + 7) / 8;
+    if (ka <= 128 && kb <= 128) {
+        const int TB = (kb + 7) / 8;
+        const int NT = (d_A == d_B && ka == kb) ? TA * (TA + 1) / 2 : TA * TB;
+        const int mt = (NT + GS_THREADS / 32 - 1) / (GS_THREADS / 32);
+        if (mt <= 2) return launch_gram_stage<2>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
+        if (mt <= 4) return launch_gram_stage<4>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
+        if (mt <= 8) return launch_gram_stage<8>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
+        if (mt <= 16) return launch_gram_stage<16>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
+        return launch_gram_stage<32>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
+    }
     if (TA <= 2) return launch_gram<2, 16>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
     if (TA <= 5) return launch_gram<5, 5>(d_A, d_B, n, ka, kb, d_partials, d_C, st);
     if (TA <= 8) return launch_gram<8, 4>(d_A, d_B, n, ka, kb, d_partials, d_C, st);

@@ -68,3 +68,21 @@ def test_ritz_factor_map_matches_host():
     # eigenvectors are defined up to sign
     np.testing.assert_allclose(np.abs(Wr), np.abs(ref), atol=1e-10)
     np.testing.assert_allclose(Wr @ Wr.T, ref @ ref.T, atol=1e-10)
+
+
+@pytest.mark.parametrize("n,ka,kb,same", [(1, 3, 3, True), (5, 8, 8, True), (178, 24, 24, True),
+                                          (178, 24, 24, False), (1000, 40, 16, False),
+                                          (100_003, 40, 40, True), (4099, 108, 108, True),
+                                          (777, 130, 24, False)])
+def test_gram_matches_numpy(built, n, ka, kb, same):
+    """rfxc_gram (A^T B, f64, fixed-order partial sums) against numpy."""
+    import torch
+    from paper_2511_19493_b200 import proximity as P
+    rng = np.random.default_rng(n + ka)
+    A = rng.normal(size=(n, ka))
+    B = A if same else rng.normal(size=(n, kb))
+    dA = torch.from_numpy(A).cuda()
+    dB = dA if same else torch.from_numpy(B).cuda()
+    got = P._gram(dA, dB).cpu().numpy()
+    want = A.T @ B
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
