@@ -7,8 +7,10 @@ timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -3
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -1 gpurun_out/bench_ref.json | cut -c1-300
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.out 2>&1
-python scripts/launch_summary.py gpurun_out/launches.csv 5 | head -12
-for k in ${KERNELS:-sketch_phase_kernel mds_kernel traverse_kernel bucket_kernel}; do
-  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -s 2 -c 1 -o gpurun_out/full_$k -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+python scripts/launch_summary.py gpurun_out/launches.csv 8 | head -14 | tee gpurun_out/launches_summary.txt
+for k in ${KERNELS:-sketch_phase_kernel mds_kernel traverse_kernel radix_bucket_kernel}; do
+  c=1; if [ $k = sketch_phase_kernel ]; then c=2; fi
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -s 2 -c $c -o gpurun_out/full_$k -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 done
+python scripts/ncu_traffic.py gpurun_out/full_sketch_phase_kernel.ncu-rep 16 | tail -1
 ls gpurun_out/*.ncu-rep
