@@ -727,7 +727,10 @@ __device__ __forceinline__ void slot_combine(float4& a, int R, int k4, int slot,
 
 // Per-warp shared scratch: SKP_RMAX x 32 uint32 (phase A perm values /
 // phase B leaf-sum row ids).
-constexpr int SKP_SCRATCH = SKP_RMAX * 32;
+// slot stride 36 words: the slots' same-position entries fall in different
+// bank groups (a stride of 32 made every slot read hit the same bank)
+constexpr int SKP_SLOT = 36;
+constexpr int SKP_SCRATCH = SKP_RMAX * SKP_SLOT;
 constexpr int SKP_UA = 4;
 #ifndef SKP_MINB_A
 #define SKP_MINB_A 3
@@ -792,7 +795,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
         for (int j = 0; j < SKP_RMAX; j++) {
             mm[j] = (int)max64(0, min64(32, P1 - (P0 + 32 * (int64_t)(s0 + j))));
             fl[j] = __ballot_sync(0xffffffffu, lane < mm[j] && (pv[j] & RFXC_PERM_FIRST));
-            pbuf[j * 32 + lane] = (pv[j] & ~RFXC_PERM_FIRST) * (uint32_t)k4;  // row offset in float4
+            pbuf[j * SKP_SLOT + lane] = (pv[j] & ~RFXC_PERM_FIRST) * (uint32_t)k4;  // row offset in float4
         }
         if (s0 == 0 && (fl[0] & 1u)) { ckind = 0; }  // the item starts a leaf
         __syncwarp();
@@ -814,7 +817,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
         int cur = he ? skp_leaf_at(A.seg, g0, gN, q0) : gi + before + ((fs & 1u) && !first_sub ? 1 : 0);
         bool inside = (fs & 1u) != 0;  // current segment started inside this sub-chunk
         float4 acc = z4, head = z4;
-        const uint32_t* pb = pbuf + (on ? slot : 0) * 32;  // idle lanes shadow slot 0
+        const uint32_t* pb = pbuf + (on ? slot : 0) * SKP_SLOT;  // idle lanes shadow slot 0
         const char* xb = reinterpret_cast<const char*>(X4 + c4);
         // leaf starts at p in (0, m)
         const unsigned fsx = (fs & ~1u) & (m >= 32 ? 0xffffffffu : ((1u << m) - 1u));
@@ -942,7 +945,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
     const int64_t i0 = it * SKP_SAMPLES, i1 = min64(i0 + SKP_SAMPLES, A.n);
     const int32_t lb = lane < nT ? (int32_t)(A.leaf_base[b0 + lane] - g0) : 0;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int* rb = reinterpret_cast<const int*>(rbuf) + slot * 32;
+    const int* rb = reinterpret_cast<const int*>(rbuf) + (on ? slot : 0) * SKP_SLOT;
 
     int32_t cn[SKP_RMAX];
     auto load_codes = [&](int64_t ib) {
@@ -955,7 +958,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
     load_codes(i0);
     for (int64_t ib = i0; ib < i1; ib += R) {
 #pragma unroll
-        for (int j = 0; j < SKP_RMAX; j++) reinterpret_cast<int*>(rbuf)[j * 32 + lane] = lb + cn[j];
+        for (int j = 0; j < SKP_RMAX; j++) reinterpret_cast<int*>(rbuf)[j * SKP_SLOT + lane] = lb + cn[j];
         __syncwarp();
         if (ib + R < i1) load_codes(ib + R);
         const int64_t i = ib + slot;
