@@ -296,6 +296,19 @@ int rfxc_gram_matvec(const double* d_dq, int64_t n, int32_t r, double pmax,
                      const double* d_v, double* d_w, void* d_work,
                      void* stream);
 
+/* ------------------------------------------------------- outlier scores */
+/* outlier_scores (proximity.py:432-485): score_i = mean over j != i of
+ * 1 / max(p_ij, floor)^2.  FullTriangle: d_packed is the packed f64 upper
+ * triangle (n(n-1)/2), d_work rfxc_outlier_work_bytes(n) bytes.  Low rank:
+ * p_ij = clip(dq_i . dq_j, 0, 1) over the (n, r) f64 dequantised factor,
+ * the diagonal term subtracted from the full row sum (:475-479).  Fixed-order
+ * sums (bit-reproducible).  n >= 2, floor > 0, r <= ~100. */
+int64_t rfxc_outlier_work_bytes(int64_t n);
+int rfxc_outlier_packed(const double* d_packed, int64_t n, double floor_,
+                        double* d_scores, void* d_work, void* stream);
+int rfxc_outlier_lowrank(const double* d_dq, int64_t n, int32_t r, double floor_,
+                         double* d_scores, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -174,12 +174,21 @@ class FullTriangle:
     n: int
     tree_count: int
     packed: np.ndarray
+    _packed_dev: object = field(default=None, repr=False, compare=False)  # HBM copy (K3 output)
 
     def entry(self, i: int, j: int) -> float:
         i, j = _check_pair(self.n, i, j)
         if i == j:
             return 1.0
         return float(self.packed[packed_index(self.n, i, j)])
+
+    def packed_device(self):
+        """The packed triangle in HBM (kept from full_proximity, else uploaded)."""
+        import torch
+        if self._packed_dev is None:
+            self._packed_dev = torch.from_numpy(np.ascontiguousarray(self.packed)).to(
+                _lib.require_cuda())
+        return self._packed_dev
 
     def to_dense(self) -> np.ndarray:
         dense = np.empty((self.n, self.n), dtype=np.float64)
@@ -240,7 +249,8 @@ def full_proximity(membership: LeafMembership,
         return FullTriangle(n=n, tree_count=membership.tree_count,
                             packed=np.empty(0, dtype=np.float64))
     out = pair_counts_device(membership, _lib.UPPER_F64)
-    return FullTriangle(n=n, tree_count=membership.tree_count, packed=out.cpu().numpy())
+    return FullTriangle(n=n, tree_count=membership.tree_count, packed=out.cpu().numpy(),
+                        _packed_dev=out)
 
 
 # ------------------------------------------------------------------ TriBlock
@@ -727,6 +737,62 @@ def lowrank_proximity(membership: LeafMembership, rank: int, mode: str = "i8",
     GPU (K4) and never materialised.  ``group``: torch.distributed group of
     the tree shards when ``membership`` is a shard."""
     return lowrank_device(membership, rank, mode, seed, group).to_host()
+
+
+# ------------------------------------------------------------- outlier scores
+def outlier_scores(repr_, clamp_floor: float | None = None) -> np.ndarray:
+    """Mean inverse-squared proximity of each sample to all others
+    (proximity.py:432-485): proximities clamped below at ``clamp_floor``
+    (default 1/B).  FullTriangle and LowRankQuantized run on the GPU
+    (rfxc_outlier_packed / rfxc_outlier_lowrank, n^2 r on the FP64 tensor
+    cores for the factor); a TriBlock's tiers are host arrays by contract, so
+    its O(pairs) scatter stays the reference's host epilogue."""
+    import torch
+    n = repr_.n
+    if n < 2:
+        raise RfxError("outlier scores need n >= 2")
+    floor = 1.0 / repr_.tree_count if clamp_floor is None else clamp_floor
+    if floor <= 0:
+        raise RfxError("clamp_floor must be positive")
+    if isinstance(repr_, FullTriangle):
+        packed = repr_.packed_device()
+        work = torch.empty(int(_lib.load().rfxc_outlier_work_bytes(n)), dtype=torch.uint8,
+                           device=packed.device)
+        scores = torch.empty(n, dtype=torch.float64, device=packed.device)
+        with region("outlier"):
+            _lib.call("rfxc_outlier_packed", _lib.ptr(packed), n, float(floor), _lib.ptr(scores),
+                      _lib.ptr(work), _lib.stream_handle())
+        return scores.cpu().numpy()
+    if isinstance(repr_, TriBlock):
+        scores = np.zeros(n, dtype=np.float64)
+        base = 1.0 / floor**2
+        scores[:] = (n - 1) * base
+        d = repr_.dense
+        if repr_.dense_count:
+            if isinstance(d, PairMap):
+                di, dj, dv = d.i, d.j, d.v
+            else:  # any Mapping {(i, j): v}, as proximity.py:455-466 reads it
+                keys = list(d.keys())
+                di = np.fromiter((k[0] for k in keys), dtype=np.int64, count=len(keys))
+                dj = np.fromiter((k[1] for k in keys), dtype=np.int64, count=len(keys))
+                dv = np.fromiter((d[k] for k in keys), dtype=np.float64, count=len(keys))
+            adj = 1.0 / np.maximum(dv, floor) ** 2 - base
+            np.add.at(scores, di, adj)
+            np.add.at(scores, dj, adj)
+        if repr_.sparse_count:
+            adj = 1.0 / np.maximum(repr_.sparse_v, floor) ** 2 - base
+            np.add.at(scores, repr_.sparse_i, adj)
+            np.add.at(scores, repr_.sparse_j, adj)
+        return scores / (n - 1)
+    if isinstance(repr_, LowRankQuantized):
+        dq = repr_.dequantized_device()
+        r = int(dq.shape[1])
+        scores = torch.empty(n, dtype=torch.float64, device=dq.device)
+        with region("outlier"):
+            _lib.call("rfxc_outlier_lowrank", _lib.ptr(dq), n, r, float(floor), _lib.ptr(scores),
+                      _lib.stream_handle())
+        return scores.cpu().numpy()
+    raise RfxError(f"unknown proximity representation {type(repr_)!r}")
 
 
 # ------------------------------------------------------------------ accessors

@@ -11,6 +11,7 @@ downstream code type-checks: ``mds.mds_full`` ``mds.py:100-101``,
   rfx.proximity.full_proximity      proximity.py:188-201
   rfx.proximity.triblock_proximity  proximity.py:275-327
   rfx.proximity.lowrank_proximity   proximity.py:367-420
+  rfx.proximity.outlier_scores      proximity.py:432-485
   rfx.mds.gram_matvec               mds.py:161-181
   rfx.mds.mds_lowrank               mds.py:184-268
 
@@ -34,7 +35,7 @@ from .quantize import QuantFactor as _QuantFactor
 
 PATCHED = {
     "proximity": ("leaf_membership", "full_proximity", "triblock_proximity",
-                  "lowrank_proximity"),
+                  "lowrank_proximity", "outlier_scores"),
     "mds": ("gram_matvec", "mds_lowrank"),
 }
 
@@ -119,6 +120,20 @@ def install(rfx=None):
                                    rank_degraded=out.rank_degraded)
 
     @tr
+    def outlier_scores(repr_, clamp_floor=None):
+        if isinstance(repr_, RP.FullTriangle):
+            mine = _prox.FullTriangle(n=repr_.n, tree_count=repr_.tree_count, packed=repr_.packed)
+        elif isinstance(repr_, RP.TriBlock):
+            mine = _prox.TriBlock(n=repr_.n, tree_count=repr_.tree_count, tau=repr_.tau,
+                                  dense=repr_.dense, sparse_i=repr_.sparse_i,
+                                  sparse_j=repr_.sparse_j, sparse_v=repr_.sparse_v)
+        elif isinstance(repr_, RP.LowRankQuantized):
+            mine = _ours_lowrank(repr_)
+        else:
+            mine = repr_
+        return _prox.outlier_scores(mine, clamp_floor)
+
+    @tr
     def gram_matvec(lowrank, v):
         return _mds.gram_matvec(_ours_lowrank(lowrank), v)
 
@@ -133,7 +148,8 @@ def install(rfx=None):
 
     new = {"proximity": {"leaf_membership": leaf_membership, "full_proximity": full_proximity,
                          "triblock_proximity": triblock_proximity,
-                         "lowrank_proximity": lowrank_proximity},
+                         "lowrank_proximity": lowrank_proximity,
+                         "outlier_scores": outlier_scores},
            "mds": {"gram_matvec": gram_matvec, "mds_lowrank": mds_lowrank}}
     for modname, names in PATCHED.items():
         mod = getattr(rfx, modname)
