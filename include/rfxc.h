@@ -118,6 +118,15 @@ int rfxc_leaf_codes(const void* d_nodes, const int64_t* d_node_off,
 int rfxc_transpose_i32(const int32_t* d_in, int64_t rows, int64_t cols,
                        int32_t* d_out, void* stream);
 
+/* OOB votes (oob_votes_tree, _kernels.py:377-385; forest.py:287-290) from
+ * the leaf codes: d_votes (n, C) int64 = #{trees b with d_inbag[b, i] == 0
+ * whose leaf of sample i has class c}.  d_leaf_class: class of every leaf
+ * (node_class of the terminal nodes in node order), indexed by
+ * d_leaf_base[b] + code; d_inbag (Bl, n) int32 bootstrap counts. */
+int rfxc_oob_votes(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
+                   const int64_t* d_leaf_base, const int32_t* d_leaf_class,
+                   const int32_t* d_inbag, int32_t C, int64_t* d_votes, void* stream);
+
 /* -------------------------------------------------------------------- K2 */
 /* Stable per-tree sort of samples by leaf (the counting sort inside
  * accumulate_pair_counts[_block], _kernels.py:458-468, :491-501), done once

@@ -338,3 +338,53 @@ extern "C" int rfxc_transpose_i32(const int32_t* d_in, int64_t rows, int64_t col
     transpose_i32_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(d_in, rows, cols, d_out);
     return check_launch("transpose_i32");
 }
+
+// ------------------------------------------------------------- OOB votes
+// the out-of-bag votes the trainer accumulates
+// (oob_votes_tree, _kernels.py:377-385, called per tree in forest.py:287-290)
+// recomputed from the K1 leaf codes: votes[i, class(leaf_b(i))] += 1 for every
+// tree b with inbag[b, i] == 0.  A thread per sample walks the trees in order
+// (coalesced codes / inbag rows); counts up to OOB_LOCAL classes stay in
+// registers, more use integer atomics (order-free, exact).
+constexpr int OOB_LOCAL = 16;
+
+__global__ void oob_votes_kernel(const int32_t* __restrict__ codes_tm, int64_t n, int Bl,
+                                 const int64_t* __restrict__ leaf_base,
+                                 const int32_t* __restrict__ leaf_class,
+                                 const int32_t* __restrict__ inbag, int C,
+                                 long long* __restrict__ votes)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    long long loc[OOB_LOCAL];
+#pragma unroll
+    for (int c = 0; c < OOB_LOCAL; c++) loc[c] = 0;
+    for (int b = 0; b < Bl; b++) {
+        if (__ldg(inbag + (int64_t)b * n + i) != 0) continue;
+        const int cls = __ldg(leaf_class + __ldg(leaf_base + b) + __ldg(codes_tm + (int64_t)b * n + i));
+        if (C <= OOB_LOCAL) {
+#pragma unroll
+            for (int c = 0; c < OOB_LOCAL; c++) loc[c] += (c == cls);
+        } else {
+            atomicAdd(reinterpret_cast<unsigned long long*>(votes + i * C + cls), 1ull);
+        }
+    }
+    if (C <= OOB_LOCAL)
+        for (int c = 0; c < C; c++) votes[i * C + c] = loc[c];
+}
+
+extern "C" int rfxc_oob_votes(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
+                              const int64_t* d_leaf_base, const int32_t* d_leaf_class,
+                              const int32_t* d_inbag, int32_t C, int64_t* d_votes, void* stream)
+{
+    if (n < 1 || Bl < 1 || C < 1) return fail(RFXC_EDATA, "oob_votes: bad shape");
+    cudaStream_t st = as_stream(stream);
+    if (C > OOB_LOCAL) {
+        const cudaError_t e = cudaMemsetAsync(d_votes, 0, (size_t)n * C * 8, st);
+        if (e != cudaSuccess) return fail(RFXC_ECUDA, "oob_votes memset: %s", cudaGetErrorString(e));
+    }
+    oob_votes_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+        d_codes_tm, n, Bl, d_leaf_base, d_leaf_class, d_inbag, C,
+        reinterpret_cast<long long*>(d_votes));
+    return check_launch("oob_votes");
+}

@@ -166,6 +166,33 @@ def leaf_membership(forest, dataset, trees: tuple | None = None) -> LeafMembersh
 
 
 # ------------------------------------------------------------- full triangle
+def oob_votes(forest, dataset, membership: "LeafMembership | None" = None) -> np.ndarray:
+    """Out-of-bag class votes (n, C) int64 recomputed on the GPU from the K1
+    leaf codes — the accumulation the trainer does per tree
+    (oob_votes_tree, _kernels.py:377-385; forest.py:287-290), so it must
+    equal ``forest.oob_votes`` exactly."""
+    import torch
+    mem = membership if membership is not None else leaf_membership(forest, dataset)
+    d = mem.device()
+    if d.is_shard:
+        raise DataError("oob votes need every tree of the forest")
+    counts = np.ascontiguousarray(forest.bootstrap.counts, dtype=np.int32)
+    if counts.shape != (d.B, d.n):
+        raise DataError(f"bootstrap counts {counts.shape} do not match (B, n) = ({d.B}, {d.n})")
+    leaf_class = np.concatenate([np.asarray(t.node_class)[np.asarray(t.status) == 1]
+                                 for t in forest.trees]).astype(np.int32)
+    if leaf_class.size != d.total_leaves:
+        raise DataError("leaf classes do not match the membership's leaf counts")
+    C = int(forest.class_count)
+    dev = d.codes_tm.device
+    lc = torch.from_numpy(leaf_class).to(dev)
+    inbag = torch.from_numpy(counts).to(dev)
+    votes = torch.empty((d.n, C), dtype=torch.int64, device=dev)
+    _lib.call("rfxc_oob_votes", _lib.ptr(d.codes_tm), d.n, d.B, _lib.ptr(d.leaf_base),
+              _lib.ptr(lc), _lib.ptr(inbag), C, _lib.ptr(votes), _lib.stream_handle())
+    return votes.cpu().numpy()
+
+
 @dataclass
 class FullTriangle:
     """Exact proximities, packed upper triangle, implicit unit diagonal

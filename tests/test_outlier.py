@@ -1,4 +1,5 @@
-"""outlier_scores (proximity.py:432-485), SURVEY §8(f) rank 1.
+"""SURVEY §8(f) epilogues: outlier_scores (proximity.py:432-485, rank 1)
+and the OOB votes recomputed from the leaf codes (rank 4, last test).
 
 CPU: the oracle restatement against the reference's own scores
 (tests/golden/outlier_wine50.npz, tests/golden/make_outlier_golden.py).
@@ -87,3 +88,15 @@ def test_full_triangle_device_copy_vs_oracle(synth2k):
     for floor in (None, 0.1):
         want = orc.outlier_packed(full.packed, full.n, 1 / 40 if floor is None else floor)
         np.testing.assert_allclose(P.outlier_scores(full, clamp_floor=floor), want, rtol=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")
+def test_oob_votes_equal_the_trainers(wine50, wine_ds, synth2k):
+    """OOB votes from the device leaf codes equal the
+    votes the trainer accumulated (forest.oob_votes, byte-identical to the
+    reference's RFX1 record, tests/test_train.py)."""
+    from paper_2511_19493_b200 import proximity as P
+    for forest, ds in ((wine50, wine_ds), synth2k[::-1]):
+        got = P.oob_votes(forest, ds)
+        assert got.dtype == np.int64 and np.array_equal(got, forest.oob_votes)
