@@ -115,12 +115,18 @@ __global__ void pack_kernel(const int8_t* __restrict__ status,
 }
 
 // ------------------------------------------------------------ K1 traverse
-constexpr int TRAV_T = 128;   // samples per CTA (one X row each in shared memory)
-constexpr int TRAV_G = 8;     // tree groups per CTA: TRAV_T * TRAV_G threads share the tile
-constexpr int TRAV_ILP = 2;   // independent tree chains per thread
+#ifndef RFXC_TRAV_G
+#define RFXC_TRAV_G 8
+#endif
+#ifndef RFXC_TRAV_ILP
+#define RFXC_TRAV_ILP 2
+#endif
+constexpr int TRAV_T = 128;             // samples per CTA (one X row each in shared memory)
+constexpr int TRAV_G = RFXC_TRAV_G;     // tree groups per CTA: TRAV_T * TRAV_G threads share the tile
+constexpr int TRAV_ILP = RFXC_TRAV_ILP; // independent tree chains per thread
 
 template <int LAYOUT, bool SMEM_X>
-__global__ void __launch_bounds__(TRAV_T * TRAV_G, 2)
+__global__ void __launch_bounds__(TRAV_T * TRAV_G, 2048 / (TRAV_T * TRAV_G))
 traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ node_off,
                 int fb, int p, int tree_lo, int tree_hi, int trees_per_chunk,
                 const void* __restrict__ values_v, int64_t n,
