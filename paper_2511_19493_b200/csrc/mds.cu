@@ -227,10 +227,12 @@ __device__ void spass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows, c
 // whole upper triangle (one B fragment per column tile per k-step, the A
 // fragment is x times it, RT(RT+1)/2 DMMA chains) plus t = sum x q and
 // sum x; the four warp partials are added in warp order 3, 2, 1, 0 through
-// shared memory `buf` (>= 32 * (RT(RT+1) + RT + 1) doubles).
+// shared memory `buf` (>= 32 * (RT(RT+1) + RT + 1) doubles).  Warps >= SP_W
+// run `extra()` while the first SP_W warps multiply.
 constexpr int SP_W = 4;
-template <int RT>
-__device__ void spass4(const MdsArgs& A, const Sm& s, int64_t rows, const double* x, double* buf)
+template <int RT, typename Extra>
+__device__ void spass4(const MdsArgs& A, const Sm& s, int64_t rows, const double* x, double* buf,
+                       Extra&& extra)
 {
     constexpr int NP = RT * (RT + 1) / 2;
     constexpr int NV = 2 * NP + RT + 1;
@@ -269,6 +271,8 @@ __device__ void spass4(const MdsArgs& A, const Sm& s, int64_t rows, const double
             v[j] += __shfl_xor_sync(0xffffffffu, v[j], 1);
             v[j] += __shfl_xor_sync(0xffffffffu, v[j], 2);
         }
+    } else {
+        extra();  // the other warps do the caller's row sums meanwhile
     }
     for (int w = SP_W - 1; w >= 1; w--) {
         if (warp == w) {
@@ -339,17 +343,17 @@ __device__ void final_a(const MdsArgs& A, int entries, const int* tab)
     const int dm = A.NT * 64 + XS_DMAX;
     const int r = A.r, SL = A.RPs + 4;
     if (gw >= entries) return;
-    // mean(v) from the sum slot (same order as its own entry below)
-    double sv = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) sv += A.sparts[(int64_t)b * A.PE + A.NT * 64 + XS_SUM];
-    const double mean = warp_sum(sv) / (double)A.n;
     for (int e = gw; e < entries; e += nw) {
-        double v = 0.0;
+        // the entry and mean(v) (the sum slot, in its own entry's order) from
+        // one pass over the CTA partials
+        double v = 0.0, sv = 0.0;
         for (int b = lane; b < (int)gridDim.x; b += 32) {
             const double x = A.sparts[(int64_t)b * A.PE + e];
+            sv += A.sparts[(int64_t)b * A.PE + A.NT * 64 + XS_SUM];
             v = (e == dm) ? fmax(v, x) : v + x;
         }
         v = (e == dm) ? warp_max(v) : warp_sum(v);
+        const double mean = warp_sum(sv) / (double)A.n;
         if (lane != 0) continue;
         A.tot[e] = v;
         if (e >= A.NT * 64 || !A.sc) continue;
@@ -622,14 +626,23 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     int par = 0;
     const int EA = A.NT * 64 + XA;
 
-    auto sreduce = [&]() {
-        if constexpr (QS == QS_F64 && SMS && RT >= 2 && RT <= 4) spass4<RT>(A, s, rows, s.us, s.S);
-        else spass<QS>(A, s, r0, rows, s.us);
+    constexpr bool SP4 = QS == QS_F64 && SMS && RT >= 2 && RT <= 4;
+    // S' reduction of s.us; `extra(t0, stride)` (row sums over rows t0, t0 +
+    // stride, ...) runs on the warps the reduction leaves idle
+    auto sreduce = [&](auto&& extra) {
+        if constexpr (SP4) {
+            spass4<RT>(A, s, rows, s.us, s.S, [&]() {
+                extra((int)threadIdx.x - 32 * SP_W, (int)blockDim.x - 32 * SP_W);
+            });
+        } else {
+            spass<QS>(A, s, r0, rows, s.us);
+            extra((int)threadIdx.x, (int)blockDim.x);
+        }
     };
     // constants C' = sum q' q'^T (u = 1)
     for (int64_t i = threadIdx.x; i < rows; i += (int)blockDim.x) s.us[i] = 1.0;
     __syncthreads();
-    sreduce();
+    sreduce([](int, int) {});
     grid.sync();
     {
         const int lane = threadIdx.x & 31;
@@ -686,22 +699,23 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     unsigned long long t_last = gtime();
     auto reduce_a = [&](int nf, double dmax_local) {
         MDS_T(0);
-        sreduce();
-        MDS_T(1);
         double x[XS_DI + 1];
 #pragma unroll
         for (int j = 0; j <= XS_DI; j++) x[j] = 0.0;
-        for (int64_t i = threadIdx.x; i < rows; i += (int)blockDim.x) {
-            const double vi = s.us[i];
-            x[XS_SUM] += vi;
+        sreduce([&](int t0, int stride) {
+            for (int64_t i = t0; i < rows; i += stride) {
+                const double vi = s.us[i];
+                x[XS_SUM] += vi;
 #pragma unroll
-            for (int f = 0; f < 8; f++)
-                if (f < nf) x[XS_D + f] += A.V[(int64_t)f * n + r0 + i] * vi;
-            if (SMS) {
-                x[XS_CI] += A.ci[r0 + i] * vi;
-                x[XS_DI] += A.di[r0 + i] * vi;
+                for (int f = 0; f < 8; f++)
+                    if (f < nf) x[XS_D + f] += A.V[(int64_t)f * n + r0 + i] * vi;
+                if (SMS) {
+                    x[XS_CI] += A.ci[r0 + i] * vi;
+                    x[XS_DI] += A.di[r0 + i] * vi;
+                }
             }
-        }
+        });
+        MDS_T(1);
         double* out = A.sparts + (int64_t)blockIdx.x * A.PE + A.NT * 64;
         block_sums(x, XS_DI + 1, s.red, s.bc);
         const double dm = block_max(dmax_local, s.red);
