@@ -646,7 +646,7 @@ def orthonormalize(Y, ld: int):
 
 
 LINALG_MAX_K = 110  # one-CTA k x k kernels (csrc/linalg.cu)
-RITZ_ON_DEVICE = False
+RITZ_ON_DEVICE = os.environ.get("RFX_RITZ_ON_DEVICE", "0") == "1"
 
 
 def _orthonormalize_host(Y, ld: int):
