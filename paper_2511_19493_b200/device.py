@@ -66,6 +66,51 @@ UPLOAD_CHUNK_TREES = 128
 _COPY_STREAMS: dict = {}
 
 
+D2H_CHUNK = 64 << 20  # bytes per staged chunk
+_D2H_RING = {}
+
+
+def host_copy(t):
+    """numpy copy of a device tensor.  Large results stream through a reused
+    pair of pinned staging buffers on the copy stream (full-rate DMA), each
+    chunk moved into the pageable destination by torch's threaded host copy
+    while the next chunk is in flight — no multi-GB pinned allocation and no
+    staged pageable cudaMemcpy."""
+    torch = _torch()
+    nbytes = t.numel() * t.element_size()
+    if nbytes < 2 * D2H_CHUNK:
+        return t.cpu().numpy()
+    key = str(t.device)
+    if key not in _D2H_RING:
+        _D2H_RING[key] = [torch.empty(D2H_CHUNK, dtype=torch.uint8, pin_memory=True)
+                          for _ in range(2)]
+    ring = _D2H_RING[key]
+    src = t.contiguous().view(-1).view(torch.uint8)
+    out = np.empty(t.shape, dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    dst = torch.from_numpy(out.reshape(-1).view(np.uint8))
+    cs = _copy_stream(t.device)
+    cs.wait_stream(torch.cuda.current_stream())
+    spans = [(a, min(nbytes, a + D2H_CHUNK)) for a in range(0, nbytes, D2H_CHUNK)]
+    events = []
+
+    def issue(k):
+        a, b = spans[k]
+        with torch.cuda.stream(cs):
+            ring[k % 2][:b - a].copy_(src[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        events.append(ev)
+
+    issue(0)
+    for k, (a, b) in enumerate(spans):
+        if k + 1 < len(spans):  # its ring slot was drained by the host copy of chunk k - 1
+            issue(k + 1)
+        events[k].synchronize()
+        dst[a:b].copy_(ring[k % 2][:b - a])
+    src.record_stream(cs)
+    return out
+
+
 def _copy_stream(dev):
     torch = _torch()
     key = dev.index if dev.index is not None else torch.cuda.current_device()

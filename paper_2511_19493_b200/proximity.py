@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .device import DeviceForest, DeviceMembership, DeviceValues, traverse
+from .device import DeviceForest, DeviceMembership, DeviceValues, host_copy, traverse
 from .errors import BudgetError, DataError, RfxError
 from .profiling import region
 from .quantize import (BYTES_PER_ELEMENT, MODES, QuantFactor, dequantize,
@@ -84,7 +84,7 @@ class LeafMembership:
             if d.is_shard:
                 raise RfxError("codes of a tree shard: gather with "
                                "distributed.gather_codes(membership)")
-            self._codes = d.codes_nb.cpu().numpy()
+            self._codes = host_copy(d.codes_nb)
         return self._codes
 
     @codes.setter
@@ -276,7 +276,7 @@ def full_proximity(membership: LeafMembership,
         return FullTriangle(n=n, tree_count=membership.tree_count,
                             packed=np.empty(0, dtype=np.float64))
     out = pair_counts_device(membership, _lib.UPPER_F64)
-    return FullTriangle(n=n, tree_count=membership.tree_count, packed=out.cpu().numpy(),
+    return FullTriangle(n=n, tree_count=membership.tree_count, packed=host_copy(out),
                         _packed_dev=out)
 
 
