@@ -965,10 +965,18 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
         const bool act = on && i < i1;
         double yo[4] = {0.0, 0.0, 0.0, 0.0};
         double* y = A.Y + i * A.k + 4 * c4;
+        // k = 4 * k4: the lane's 4 doubles are 32-byte aligned -> two 16-byte accesses
+        const bool vec = K4 != 0 && A.k == 4 * k4;
         if (act && !first) {
+            if (vec) {
+                const double2 lo = __ldcs(reinterpret_cast<const double2*>(y));
+                const double2 hi = __ldcs(reinterpret_cast<const double2*>(y) + 1);
+                yo[0] = lo.x; yo[1] = lo.y; yo[2] = hi.x; yo[3] = hi.y;
+            } else {
 #pragma unroll
-            for (int q = 0; q < 4; q++)
-                if (4 * c4 + q < A.k) yo[q] = __ldcs(y + q);  // Y streams through L2
+                for (int q = 0; q < 4; q++)
+                    if (4 * c4 + q < A.k) yo[q] = __ldcs(y + q);  // Y streams through L2
+            }
         }
         float4 acc = z4;
         for (int t0 = 0; t0 < nT; t0 += SKP_UB) {
@@ -983,12 +991,19 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
         }
         if (act) {
             const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+            double v[4];
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-                if (4 * c4 + q < A.k) {
-                    const double v = yo[q] + (double)a4[q];
-                    __stcs(y + q, last ? v * A.scale : v);
-                }
+                v[q] = yo[q] + (double)a4[q];
+                if (last) v[q] *= A.scale;
+            }
+            if (vec) {
+                __stcs(reinterpret_cast<double2*>(y), make_double2(v[0], v[1]));
+                __stcs(reinterpret_cast<double2*>(y) + 1, make_double2(v[2], v[3]));
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    if (4 * c4 + q < A.k) __stcs(y + q, v[q]);
             }
         }
         __syncwarp();
