@@ -164,12 +164,45 @@ pmax_kernel(const double* __restrict__ dq, int64_t n, int r, int64_t rows_per_pa
             m = fmax(m, s);
         }
     } else {
-        if (threadIdx.x == 0) {
-            uint64_t s[2] = {s0, s1};
-            for (int t = 0; t < 1024; t++) {
-                pairs[2 * t] = (int)rfx_pcg32_bounded(s, (uint32_t)n);
-                pairs[2 * t + 1] = (int)rfx_pcg32_bounded(s, (uint32_t)n);
+        // the 2048 bounded draws of the sequential stream, generated in
+        // parallel: thread t jumps ahead to raw draw PM_PER * t, keeps the
+        // draws >= threshold (rfx_pcg32_bounded's acceptance test) and a block
+        // scan of the accept counts gives every kept draw its place in the
+        // bounded sequence; if the margin ever ran out, thread 0 redoes it
+        // sequentially (exactly the same sequence either way)
+        constexpr int PM_PER = 9;  // 256 * 9 = 2304 raw draws >= 2048 + margin
+        const uint32_t b = (uint32_t)n;
+        const uint32_t thr = (uint32_t)((0x100000000ULL - b) % b);
+        uint64_t st[2] = {s0, s1};
+        rfx_pcg32_advance(st, (uint64_t)PM_PER * threadIdx.x);
+        uint32_t raw[PM_PER];
+        int cnt = 0;
+#pragma unroll
+        for (int u = 0; u < PM_PER; u++) {
+            raw[u] = rfx_pcg32_next(st);
+            cnt += raw[u] >= thr;
+        }
+        __shared__ int scan[256];
+        scan[threadIdx.x] = cnt;
+        __syncthreads();
+        for (int o = 1; o < 256; o <<= 1) {  // inclusive Hillis-Steele scan
+            const int v = threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
+            __syncthreads();
+            scan[threadIdx.x] += v;
+            __syncthreads();
+        }
+        int pos = scan[threadIdx.x] - cnt;
+#pragma unroll
+        for (int u = 0; u < PM_PER; u++)
+            if (raw[u] >= thr) {
+                if (pos < 2048) pairs[pos] = (int)(raw[u] % b);
+                pos++;
             }
+        const bool short_ = scan[255] < 2048;
+        __syncthreads();
+        if (short_ && threadIdx.x == 0) {
+            uint64_t s[2] = {s0, s1};
+            for (int t = 0; t < 2048; t++) pairs[t] = (int)rfx_pcg32_bounded(s, b);
         }
         __syncthreads();
         for (int t = threadIdx.x; t < 1024; t += blockDim.x) {
