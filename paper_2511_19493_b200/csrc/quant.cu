@@ -22,6 +22,10 @@ __constant__ double NF4_CB[16] = {
     0.44070982933044434, 0.5626170039176941, 0.7229568362236023, 1.0};
 
 int gram_parts(int64_t n);
+}  // namespace rfxc
+extern "C" int rfxc_matmul_small(const double* d_Y, int64_t n, int32_t ka, const double* d_M,
+                                 int32_t kb, double* d_Z, float* d_Z32, int32_t ld32, void* stream);
+namespace rfxc {
 
 // F = Q @ Wr row by row; per-part column absmax.  Wr staged in shared memory
 // (SW) or read through L1 when k x r is too large.
@@ -50,6 +54,26 @@ factor_kernel(const double* __restrict__ Q, int64_t n, int k, const double* __re
             m = fmax(m, fabs(s));
         }
     }
+    cm[threadIdx.x] = (roff < rstep) ? m : 0.0;
+    __syncthreads();
+    if (threadIdx.x < r) {
+        double mm = 0.0;
+        for (int q = 0; q < rstep; q++) mm = fmax(mm, cm[q * r + threadIdx.x]);
+        colmax_parts[(int64_t)blockIdx.x * r + threadIdx.x] = mm;
+    }
+}
+
+// per-part column absmax of F (n, r): thread (row offset, column), columns fastest
+__global__ void __launch_bounds__(256)
+colmax_kernel(const double* __restrict__ F, int64_t n, int r, int64_t rows_per_part,
+              double* __restrict__ colmax_parts)
+{
+    __shared__ double cm[256];
+    const int64_t r0 = blockIdx.x * rows_per_part, r1 = min(n, r0 + rows_per_part);
+    const int c = threadIdx.x % r, rstep = blockDim.x / r, roff = threadIdx.x / r;
+    double m = 0.0;
+    if (roff < rstep)
+        for (int64_t i = r0 + roff; i < r1; i += rstep) m = fmax(m, fabs(__ldg(F + i * r + c)));
     cm[threadIdx.x] = (roff < rstep) ? m : 0.0;
     __syncthreads();
     if (threadIdx.x < r) {
@@ -239,20 +263,30 @@ extern "C" int rfxc_factor_quantize(const double* d_Q, int64_t n, int32_t k, con
     const int parts = gram_parts(n);
     const int64_t rpp = ceil_div(n, parts);
     const int threads = 256;
-    const bool sw = (size_t)k * r * 8 <= 160 * 1024;
-    const size_t smem = ((sw ? (size_t)k * r : 0) + threads) * 8;
-    if (sw) {
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        factor_kernel<true><<<parts, threads, smem, st>>>(d_Q, n, k, d_Wr, r, rpp, d_factor,
-                                                          d_colmax_parts);
+    if (k <= 128 && r <= 128) {
+        // F = Q Wr on the FP64 tensor cores (the sketch's small matmul), then
+        // the per-part column absmax
+        int rc = rfxc_matmul_small(d_Q, n, k, d_Wr, r, d_factor, nullptr, 0, stream);
+        if (rc) return rc;
+        colmax_kernel<<<parts, threads, 0, st>>>(d_factor, n, r, rpp, d_colmax_parts);
+        rc = check_launch("colmax");
+        if (rc) return rc;
     } else {
-        factor_kernel<false><<<parts, threads, smem, st>>>(d_Q, n, k, d_Wr, r, rpp, d_factor,
-                                                           d_colmax_parts);
+        const bool sw = (size_t)k * r * 8 <= 160 * 1024;
+        const size_t smem = ((sw ? (size_t)k * r : 0) + threads) * 8;
+        if (sw) {
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(factor_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+            factor_kernel<true><<<parts, threads, smem, st>>>(d_Q, n, k, d_Wr, r, rpp, d_factor,
+                                                              d_colmax_parts);
+        } else {
+            factor_kernel<false><<<parts, threads, smem, st>>>(d_Q, n, k, d_Wr, r, rpp, d_factor,
+                                                               d_colmax_parts);
+        }
+        int rc = check_launch("factor");
+        if (rc) return rc;
     }
-    int rc = check_launch("factor");
-    if (rc) return rc;
     const int64_t total = n * r;
     const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 16);
     switch (mode) {
