@@ -305,11 +305,6 @@ __global__ void gram_final_kernel(const double* __restrict__ parts, int nparts, 
 // warp owns whole 8x8 output tiles (upper tiles only when A == B), so no
 // cross-warp reduction is needed; the CTA's tiles go to parts[blk] and
 // gram_final adds the parts in block order.  Deterministic.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
-{
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -529,25 +524,25 @@ matmul_small_kernel(const double* __restrict__ Y, int64_t n, int ka, const doubl
 }
 
 // ============================================================ fused pass
-// One sketch pass Y = scale * sum_b E_b E_b^T X as a single cooperative
-// kernel.  Trees are processed in batches of T (sized so that the leaf sums
-// of two batches, X and Y stay in L2); epoch e computes the leaf sums of
-// batch e (phase A) and gathers batch e-1 into Y (phase B), then a grid
-// barrier.  Leaf sums therefore never leave L2, where the two-kernel path
-// writes all sum(L) x ld sums to HBM and gathers them back per (sample, tree).
+// One sketch pass Y = scale * sum_b E_b E_b^T X.  Trees are processed in
+// batches of T <= 32 whose leaf sums fit next to X in L2 (rfxc_sketch_plan),
+// so the leaf sums never round-trip HBM, where the two-kernel path writes all
+// sum(L) x ld sums and gathers them back per (sample, tree).  Per batch two
+// launches on one stream (phase A on an auxiliary stream when two leaf-sum
+// buffers fit, overlapping the previous batch's phase B):
 //
-// Phase A (warp item = 256 consecutive positions of the bucketed perm):
-// the 32 member rows of a sub-chunk are copied into shared memory with
-// cp.async (one row per lane, next sub-chunk in flight while this one is
-// reduced), then lanes own column pairs and walk the positions in order,
-// closing a leaf at every RFXC_PERM_FIRST flag (f64 accumulation, fixed
-// order).  Leaves cut by an item boundary leave one f64 piece per item;
-// the last piece to arrive (per-leaf counter) adds the pieces in item order
-// and writes the sum, so results are bit-reproducible.
-// Phase B (warp item = 16 samples): lane t reads the sample's code in tree
-// b0+t (one coalesced row segment of the (n, B) membership), then the T
-// leaf-sum rows are gathered as float4 lanes with f64 accumulation and
-// added to Y (scaled by 1/B in the last batch).
+// Phase A (skp_phase_a; one item of positions of the bucketed perm per
+// resident warp): three row slots of k4 float4 lanes walk 32-position
+// sub-chunks in order, gathering X rows, summing each leaf segment in f32
+// (<= 32 rows) and closing a leaf at every RFXC_PERM_FIRST flag; the slots'
+// cut segments are joined in position order in an f64 carry.  Leaves cut by
+// an item boundary leave one f64 piece per item; the last piece to arrive
+// (acq_rel per-leaf counter) adds the pieces in item order and writes the
+// sum, so results are bit-reproducible.
+// Phase B (skp_phase_b; 24 samples per warp): lane t reads the sample's code
+// in tree b0+t (one coalesced segment of the (n, B) membership), the T
+// leaf-sum rows are gathered as float4 lanes and summed in f32, and the sum
+// is added to Y in f64 (scaled by 1/B in the last batch).
 constexpr int SKP_SAMPLES = 24;  // samples per phase-B item
 constexpr int SKP_RMAX = 4;      // row slots per warp (lane groups of k4 lanes)
 constexpr int SKP_MAX_T = 32;
