@@ -23,7 +23,7 @@ for rep in range(2):
     sk = P._Sketch(dm, 40)
     if rep == 0:
         lc = dm.leaf_counts
-        print("has_empty", int(dm.has_empty.item()), "T", getattr(sk, "T", None), "s_rows",
+        print("has_empty", int(dm.has_empty.item()), "T", getattr(sk, "T", None), "nbuf", getattr(sk, "nbuf", None), "s_rows",
               getattr(sk, "s_rows", None), "leaves/tree", lc.mean(), lc.max(), flush=True)
     X32 = torch.randn((ds.n, sk.ld), dtype=torch.float32, device="cuda")
     sk.apply(X32, 40)
