@@ -114,6 +114,17 @@ int rfxc_leaf_codes(const void* d_nodes, const int64_t* d_node_off,
                     const void* d_values, int64_t n, int32_t* d_codes_tm,
                     void* stream);
 
+/* The same for samples [row_lo, row_hi) only (d_values and d_codes_tm keep
+ * their full n stride). */
+int rfxc_leaf_codes_rows(const void* d_nodes, const int64_t* d_node_off,
+                         int32_t layout, int32_t p, int32_t tree_lo, int32_t tree_hi,
+                         const void* d_values, int64_t n, int64_t row_lo, int64_t row_hi,
+                         int32_t* d_codes_tm, void* stream);
+/* Rows [row_lo, row_hi) of a column-major (n, p) host matrix (element size
+ * elem bytes) into the same rows of the device copy, stream-ordered. */
+int rfxc_h2d_rows(void* d_dst, const void* h_src, int64_t n, int64_t p, int32_t elem,
+                  int64_t row_lo, int64_t row_hi, void* stream);
+
 /* (rows, cols) int32 transpose: tm <-> nb layouts. */
 int rfxc_transpose_i32(const int32_t* d_in, int64_t rows, int64_t cols,
                        int32_t* d_out, void* stream);

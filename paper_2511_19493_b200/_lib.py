@@ -43,6 +43,8 @@ SIGNATURES = {
     "rfxc_transpose_i32": (ctypes.c_int, [P, I64, I64, P, P]),
     "rfxc_bucket_scratch_bytes": (I64, [I64, I32]),
     "rfxc_outlier_work_bytes": (I64, [I64]),
+    "rfxc_leaf_codes_rows": (ctypes.c_int, [P, P, I32, I32, I32, I32, P, I64, I64, I64, P, P]),
+    "rfxc_h2d_rows": (ctypes.c_int, [P, P, I64, I64, I32, I64, I64, P]),
     "rfxc_oob_votes": (ctypes.c_int, [P, I64, I32, P, P, P, I32, P, P]),
     "rfxc_outlier_packed": (ctypes.c_int, [P, I64, F64, P, P, P]),
     "rfxc_outlier_lowrank": (ctypes.c_int, [P, I64, I32, F64, P, P]),
@@ -123,7 +125,7 @@ LAUNCHES = {"rfxc_values_to_f32": 1, "rfxc_forest_pack": 1, "rfxc_leaf_codes": 1
             "rfxc_gram": 2, "rfxc_matmul_small": 1, "rfxc_factor_quantize": 3,
             "rfxc_dequantize": 1, "rfxc_pmax": 2, "rfxc_mds_power": 1, "rfxc_gram_matvec": 1,
             "rfxc_outlier_packed": 3, "rfxc_outlier_lowrank": 1,
-            "rfxc_oob_votes": 1}
+            "rfxc_oob_votes": 1, "rfxc_leaf_codes_rows": 1}
 launch_count = 0
 
 

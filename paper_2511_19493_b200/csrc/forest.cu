@@ -129,7 +129,7 @@ template <int LAYOUT, bool SMEM_X>
 __global__ void __launch_bounds__(TRAV_T * TRAV_G, 2048 / (TRAV_T * TRAV_G))
 traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ node_off,
                 int fb, int p, int tree_lo, int tree_hi, int trees_per_chunk,
-                const void* __restrict__ values_v, int64_t n,
+                const void* __restrict__ values_v, int64_t n, int64_t row_lo, int64_t row_hi,
                 int32_t* __restrict__ codes_tm)
 {
     using V = typename std::conditional<LAYOUT == RFXC_NODES_F32, float, double>::type;
@@ -138,9 +138,9 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
     const V* __restrict__ X = reinterpret_cast<const V*>(values_v);
     const int t = threadIdx.x % TRAV_T;   // sample within the tile
     const int grp = threadIdx.x / TRAV_T; // tree group
-    const int64_t i0 = (int64_t)blockIdx.x * TRAV_T;
+    const int64_t i0 = row_lo + (int64_t)blockIdx.x * TRAV_T;
     const int64_t i = i0 + t;
-    const bool valid = i < n;
+    const bool valid = i < row_hi;
     const int stride = p + 1;  // odd row stride spreads banks
     if (SMEM_X) {
         // coalesced: consecutive threads read consecutive samples of feature f
@@ -277,8 +277,8 @@ extern "C" int rfxc_forest_pack(const int8_t* d_status, const int32_t* d_split_v
 
 template <int LAYOUT, bool SMEM_X>
 static int launch_traverse(const void* d_nodes, const int64_t* d_node_off, int p, int tree_lo,
-                           int tree_hi, const void* d_values, int64_t n, int32_t* d_codes_tm,
-                           size_t smem, cudaStream_t st)
+                           int tree_hi, const void* d_values, int64_t n, int64_t row_lo,
+                           int64_t row_hi, int32_t* d_codes_tm, size_t smem, cudaStream_t st)
 {
     auto kern = traverse_kernel<LAYOUT, SMEM_X>;
     if (smem > 48 * 1024) {
@@ -290,7 +290,7 @@ static int launch_traverse(const void* d_nodes, const int64_t* d_node_off, int p
     const int threads = TRAV_T * TRAV_G;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
     occ = std::max(occ, 1);
-    const int64_t tiles = ceil_div(n, TRAV_T);
+    const int64_t tiles = ceil_div(row_hi - row_lo, TRAV_T);
     const int nt = tree_hi - tree_lo;
     // enough CTAs for ~6 waves; every chunk a multiple of the trees one CTA
     // walks per step (TRAV_G groups x TRAV_ILP chains)
@@ -303,8 +303,31 @@ static int launch_traverse(const void* d_nodes, const int64_t* d_node_off, int p
     chunks = (int)ceil_div(nt, per);
     dim3 grid((unsigned)tiles, (unsigned)chunks);
     kern<<<grid, threads, smem, st>>>(d_nodes, d_node_off, feature_bits(p), p, tree_lo, tree_hi,
-                                      per, d_values, n, d_codes_tm);
+                                      per, d_values, n, row_lo, row_hi, d_codes_tm);
     return check_launch("leaf_codes");
+}
+
+extern "C" int rfxc_leaf_codes_rows(const void* d_nodes, const int64_t* d_node_off,
+                                    int32_t layout, int32_t p, int32_t tree_lo, int32_t tree_hi,
+                                    const void* d_values, int64_t n, int64_t row_lo,
+                                    int64_t row_hi, int32_t* d_codes_tm, void* stream)
+{
+    if (n < 1 || p < 1 || tree_lo < 0 || tree_hi <= tree_lo)
+        return fail(RFXC_EDATA, "leaf_codes: bad shape");
+    if (row_lo < 0 || row_hi > n || row_lo >= row_hi) return fail(RFXC_EDATA, "leaf_codes: bad rows");
+    cudaStream_t st = as_stream(stream);
+    const size_t vsz = layout == RFXC_NODES_F32 ? 4 : 8;
+    const size_t smem = (size_t)TRAV_T * (p + 1) * vsz;
+    const bool use_smem = smem <= 112 * 1024;
+#define RFXC_TRAV(L, S) \
+    launch_traverse<L, S>(d_nodes, d_node_off, p, tree_lo, tree_hi, d_values, n, row_lo, row_hi, \
+                          d_codes_tm, S ? smem : 0, st)
+    if (layout == RFXC_NODES_F32)
+        return use_smem ? RFXC_TRAV(RFXC_NODES_F32, true) : RFXC_TRAV(RFXC_NODES_F32, false);
+    if (layout == RFXC_NODES_F64)
+        return use_smem ? RFXC_TRAV(RFXC_NODES_F64, true) : RFXC_TRAV(RFXC_NODES_F64, false);
+#undef RFXC_TRAV
+    return fail(RFXC_EDATA, "leaf_codes: unknown layout %d", layout);
 }
 
 extern "C" int rfxc_leaf_codes(const void* d_nodes, const int64_t* d_node_off, int32_t layout,
@@ -312,27 +335,26 @@ extern "C" int rfxc_leaf_codes(const void* d_nodes, const int64_t* d_node_off, i
                                const void* d_values, int64_t n, int32_t* d_codes_tm,
                                void* stream)
 {
-    if (n < 1 || p < 1 || tree_lo < 0 || tree_hi <= tree_lo)
-        return fail(RFXC_EDATA, "leaf_codes: bad shape");
-    cudaStream_t st = as_stream(stream);
-    const size_t vsz = layout == RFXC_NODES_F32 ? 4 : 8;
-    const size_t smem = (size_t)TRAV_T * (p + 1) * vsz;
-    const bool use_smem = smem <= 112 * 1024;
-    if (layout == RFXC_NODES_F32)
-        return use_smem ? launch_traverse<RFXC_NODES_F32, true>(d_nodes, d_node_off, p, tree_lo,
-                                                                tree_hi, d_values, n, d_codes_tm,
-                                                                smem, st)
-                        : launch_traverse<RFXC_NODES_F32, false>(d_nodes, d_node_off, p, tree_lo,
-                                                                 tree_hi, d_values, n,
-                                                                 d_codes_tm, 0, st);
-    if (layout == RFXC_NODES_F64)
-        return use_smem ? launch_traverse<RFXC_NODES_F64, true>(d_nodes, d_node_off, p, tree_lo,
-                                                                tree_hi, d_values, n, d_codes_tm,
-                                                                smem, st)
-                        : launch_traverse<RFXC_NODES_F64, false>(d_nodes, d_node_off, p, tree_lo,
-                                                                 tree_hi, d_values, n,
-                                                                 d_codes_tm, 0, st);
-    return fail(RFXC_EDATA, "leaf_codes: unknown layout %d", layout);
+    return rfxc_leaf_codes_rows(d_nodes, d_node_off, layout, p, tree_lo, tree_hi, d_values, n, 0,
+                                n, d_codes_tm, stream);
+}
+
+// rows [row_lo, row_hi) of a column-major (n, p) host matrix into the same
+// rows of its device copy (one strided DMA): lets a sample block's traversal
+// start before the rest of the values have crossed PCIe
+extern "C" int rfxc_h2d_rows(void* d_dst, const void* h_src, int64_t n, int64_t p, int32_t elem,
+                             int64_t row_lo, int64_t row_hi, void* stream)
+{
+    if (row_lo < 0 || row_hi > n || row_lo > row_hi || elem < 1)
+        return fail(RFXC_EDATA, "h2d_rows: bad range");
+    if (row_hi == row_lo) return RFXC_OK;
+    const size_t pitch = (size_t)n * elem;
+    const cudaError_t e = cudaMemcpy2DAsync(
+        static_cast<char*>(d_dst) + row_lo * elem, pitch,
+        static_cast<const char*>(h_src) + row_lo * elem, pitch, (size_t)(row_hi - row_lo) * elem,
+        (size_t)p, cudaMemcpyHostToDevice, as_stream(stream));
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "h2d_rows: %s", cudaGetErrorString(e));
+    return RFXC_OK;
 }
 
 extern "C" int rfxc_transpose_i32(const int32_t* d_in, int64_t rows, int64_t cols,

@@ -63,6 +63,7 @@ def _staged(obj, key, build):
 
 
 UPLOAD_CHUNK_TREES = 128
+UPLOAD_FIRST_TREES = 32
 _COPY_STREAMS: dict = {}
 
 
@@ -137,7 +138,7 @@ class DeviceValues:
     """Dataset.values on the GPU: f32 when every value is f32-exact (then the
     f32 node layout compares exactly), else f64."""
 
-    def __init__(self, values: np.ndarray):
+    def __init__(self, values: np.ndarray, defer: bool = False):
         torch = _torch()
         self.dev = _lib.require_cuda()
         vals = np.asfortranarray(values, dtype=np.float64)
@@ -153,19 +154,31 @@ class DeviceValues:
             return buf, bool(exact[0])
 
         buf, self.exact_f32 = _staged(values, "f32", stage)
-        self.ready = None
+        self._buf = buf
+        self.ready = None       # event: every row on the device
+        self.rows_ready = []    # (row_hi, event) for uploads issued so far
         self.f32 = None
-        if self.exact_f32:  # on the copy stream; traverse() waits for `ready`
-            dst = torch.empty(vals.size * 4, dtype=torch.uint8, device=self.dev)
-            cs = _copy_stream(self.dev)
-            cs.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(cs):
-                dst.copy_(buf, non_blocking=True)
-                self.ready = torch.cuda.Event()
-                self.ready.record(cs)
-            dst.record_stream(cs)
-            self.f32 = dst.view(torch.float32).view(self.p, self.n)
+        if self.exact_f32:  # on the copy stream; traverse() waits for the rows it reads
+            self._dst = torch.empty(vals.size * 4, dtype=torch.uint8, device=self.dev)
+            self.f32 = self._dst.view(torch.float32).view(self.p, self.n)
+            if not defer:
+                self.upload_rows(0, self.n)
         self._f64 = None
+
+    def upload_rows(self, lo: int, hi: int):
+        """Copy samples [lo, hi) (all features) on the copy stream."""
+        torch = _torch()
+        cs = _copy_stream(self.dev)
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            _lib.call("rfxc_h2d_rows", _lib.ptr(self._dst), self._buf.data_ptr(), self.n, self.p, 4,
+                      lo, hi, _lib.stream_handle())
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        self._dst.record_stream(cs)
+        self.rows_ready.append((hi, ev))
+        if hi >= self.n:
+            self.ready = ev
 
     @property
     def f64(self):
@@ -180,7 +193,7 @@ class DeviceForest:
     current GPU (packed on the host, uploaded once)."""
 
     def __init__(self, forest, tree_lo: int = 0, tree_hi: int | None = None,
-                 layout: int | None = None, nthreads: int = 0):
+                 layout: int | None = None, nthreads: int = 0, defer: bool = False):
         torch = _torch()
         dev = _lib.require_cuda()
         trees = forest.trees[tree_lo:(len(forest.trees) if tree_hi is None else tree_hi)]
@@ -234,20 +247,30 @@ class DeviceForest:
         self._staging = buf
         self._nodes = torch.empty(max(self.total_nodes * rec, 1), dtype=torch.uint8, device=dev)
         # node records cross PCIe in tree chunks on a copy stream, so the
-        # traversal of chunk c overlaps the copy of chunk c + 1 (traverse())
+        # traversal of chunk c overlaps the copy of chunk c + 1 (traverse());
+        # a small first chunk lets the traversal start early
+        bounds = [0] + [c for c in range(UPLOAD_FIRST_TREES, B, UPLOAD_CHUNK_TREES)] + [B]
+        bounds = sorted(set(b_ for b_ in bounds if 0 <= b_ <= B))
+        self._spans = list(zip(bounds[:-1], bounds[1:]))
         self.chunks = []
-        step = UPLOAD_CHUNK_TREES
-        cs = _copy_stream(dev)
+        if not defer:
+            for j in range(len(self._spans)):
+                self.upload_chunk(j)
+
+    def upload_chunk(self, j: int):
+        """Copy the node records of tree chunk j on the copy stream."""
+        torch = _torch()
+        c0, c1 = self._spans[j]
+        off, rec, buf = self.node_off_host, self._rec, self._staging
+        cs = _copy_stream(self._nodes.device)
         cs.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(cs):
-            for c0 in range(0, B, step):
-                c1 = min(B, c0 + step)
-                a, b = int(off[c0]) * rec, int(off[c1]) * rec
-                self._nodes[a:b].copy_(buf[a:b], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(cs)
-                self.chunks.append((c0, c1, ev))
+            a, b = int(off[c0]) * rec, int(off[c1]) * rec
+            self._nodes[a:b].copy_(buf[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
         self._nodes.record_stream(cs)
+        self.chunks.append((c0, c1, ev))
 
     @property
     def nodes(self):
@@ -376,15 +399,25 @@ def traverse(dforest: DeviceForest, dvalues: DeviceValues):
     dev = vals.device
     tm = torch.empty((Bl, n), dtype=torch.int32, device=dev)
     cur = torch.cuda.current_stream()
-    if dvalues.ready is not None:
-        cur.wait_event(dvalues.ready)
-    done = []  # (c0, c1, event after the chunk's codes): K2 starts per chunk
+    f32_rows = dvalues.rows_ready if layout == _lib.NODES_F32 else []
+    done = []  # (c0, c1, event after the chunk's codes)
     with region("leaf_codes"):
-        for c0, c1, ev in dforest.chunks:  # each chunk after its node records arrived
+        for j, (c0, c1, ev) in enumerate(dforest.chunks):  # after its node records arrived
             cur.wait_event(ev)
-            _lib.call("rfxc_leaf_codes", _lib.ptr(dforest._nodes), _lib.ptr(dforest.node_off),
-                      layout, dvalues.p, c0, c1, _lib.ptr(vals), n, _lib.ptr(tm[c0:c1]),
-                      _lib.stream_handle())
+            # the first chunk walks each sample block as soon as its rows
+            # have arrived; later chunks need every row
+            blocks = [(lo, hi, e) for (lo, (hi, e)) in zip([0] + [h for h, _ in f32_rows],
+                                                            f32_rows)] if j == 0 else []
+            if not blocks:
+                if dvalues.ready is not None:
+                    cur.wait_event(dvalues.ready)
+                blocks = [(0, n, None)]
+            for lo, hi, e in blocks:
+                if e is not None:
+                    cur.wait_event(e)
+                _lib.call("rfxc_leaf_codes_rows", _lib.ptr(dforest._nodes),
+                          _lib.ptr(dforest.node_off), layout, dvalues.p, c0, c1, _lib.ptr(vals),
+                          n, lo, hi, _lib.ptr(tm[c0:c1]), _lib.stream_handle())
             cev = torch.cuda.Event()
             cev.record(cur)
             done.append((c0, c1, cev))
