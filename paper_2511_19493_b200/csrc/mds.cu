@@ -345,7 +345,8 @@ __device__ void final_a(const MdsArgs& A, int entries, const int* tab)
     if (gw >= entries) return;
     for (int e = gw; e < entries; e += nw) {
         // the entry and mean(v) (the sum slot, in its own entry's order) from
-        // one pass over the CTA partials
+        // one pass over the CTA partials; C' of the entry fetched alongside
+        const double ce = (lane == 0 && e < A.NT * 64) ? A.cst[e] : 0.0;
         double v = 0.0, sv = 0.0;
         for (int b = lane; b < (int)gridDim.x; b += 32) {
             const double x = A.sparts[(int64_t)b * A.PE + e];
@@ -360,7 +361,7 @@ __device__ void final_a(const MdsArgs& A, int entries, const int* tab)
         // S'(v) entry -> mean-corrected S, t or su
         const int t = e >> 6, ta = tab[2 * t], tb = tab[2 * t + 1];
         const int a = 8 * ta + ((e >> 3) & 7), b = 8 * tb + (e & 7);
-        const double c = v - mean * A.cst[e];
+        const double c = v - mean * ce;
         if (a < r && b < r) {
             A.sc[a * SL + b] = c;
             if (ta != tb) A.sc[b * SL + a] = c;
