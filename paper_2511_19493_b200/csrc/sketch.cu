@@ -725,7 +725,7 @@ __device__ __forceinline__ void slot_combine(float4& a, int R, int k4, int slot,
 // slot stride 36 words: the slots' same-position entries fall in different
 // bank groups (a stride of 32 made every slot read hit the same bank)
 constexpr int SKP_SLOT = 36;
-constexpr int SKP_SCRATCH = SKP_RMAX * SKP_SLOT;
+constexpr int SKP_SCRATCH = SKP_RMAX * SKP_SLOT + 2 * 32 * 4;  // + head/tail float4 per lane
 constexpr int SKP_UA = 4;
 #ifndef SKP_MINB_A
 #define SKP_MINB_A 3
@@ -811,7 +811,11 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
         const int64_t q0 = P0 + 32 * (int64_t)(s0 + slot);
         int cur = he ? skp_leaf_at(A.seg, g0, gN, q0) : gi + before + ((fs & 1u) && !first_sub ? 1 : 0);
         bool inside = (fs & 1u) != 0;  // current segment started inside this sub-chunk
-        float4 acc = z4, head = z4;
+        float4 acc = z4;
+        // this slot's head (segment before its first leaf start) and tail go
+        // through shared memory to the join (one 16-byte access per lane)
+        float4* hsm = reinterpret_cast<float4*>(pbuf + SKP_RMAX * SKP_SLOT);
+        float4* tsm = hsm + 32;
         const uint32_t* pb = pbuf + (on ? slot : 0) * SKP_SLOT;  // idle lanes shadow slot 0
         const char* xb = reinterpret_cast<const char*>(X4 + c4);
         // leaf starts at p in (0, m)
@@ -820,7 +824,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
             if (inside) {
                 if (on) Sb[(uint32_t)(cur - g0) * k4 + c4] = acc;
             } else {
-                head = acc;
+                hsm[lane] = acc;
             }
             cur = he ? skp_leaf_at(A.seg, g0, gN, q0 + p) : cur + 1;
             inside = true;
@@ -869,19 +873,14 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
                 }
             }
         }
+        tsm[lane] = acc;
+        __syncwarp();
         // join the slots' cut segments in position order (uniform over the warp)
 #pragma unroll
         for (int j = 0; j < SKP_RMAX; j++) {
             if (j >= R || s0 + j >= nsub) break;
             const int src = j * k4 + c4;
-            const float4 hj = make_float4(__shfl_sync(0xffffffffu, head.x, src),
-                                          __shfl_sync(0xffffffffu, head.y, src),
-                                          __shfl_sync(0xffffffffu, head.z, src),
-                                          __shfl_sync(0xffffffffu, head.w, src));
-            const float4 tj = make_float4(__shfl_sync(0xffffffffu, acc.x, src),
-                                          __shfl_sync(0xffffffffu, acc.y, src),
-                                          __shfl_sync(0xffffffffu, acc.z, src),
-                                          __shfl_sync(0xffffffffu, acc.w, src));
+            const float4 tj = tsm[src];
             const int curj = __shfl_sync(0xffffffffu, cur, j * k4);
             const unsigned fj = (s0 == 0 && j == 0) ? (fl[j] & ~1u) : fl[j];
             const bool starts = (fl[j] & 1u) != 0;
@@ -894,6 +893,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
                 continue;
             }
             if (!starts) {  // head rows close the carried leaf
+                const float4 hj = hsm[src];
                 cy[0] += (double)hj.x;
                 cy[1] += (double)hj.y;
                 cy[2] += (double)hj.z;
