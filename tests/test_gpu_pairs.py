@@ -178,3 +178,27 @@ def test_radix_bucket_edge_cases(built, n, L, mode):
         any_empty |= bool((cnt == 0).any())
     assert seg[-1] == B * n
     assert bool(int(d.has_empty.item())) == any_empty
+
+
+def test_bucket_tree_ranges_compose(synth2k):
+    """rfxc_bucket_trees over [0, a) then [a, Bl) writes exactly what one call
+    over [0, Bl) writes (perm, run starts, empty flag)."""
+    import torch
+    from paper_2511_19493_b200 import _lib
+    ds, forest = synth2k
+    d = P.leaf_membership(forest, ds).device()
+    perm, seg = d.buckets()
+    n, Bl = d.n, d.Bl
+    p2 = torch.empty_like(perm)
+    s2 = torch.empty_like(seg)
+    he = torch.zeros(1, dtype=torch.int32, device=perm.device)
+    lib = _lib.load()
+    maxl = int(d.leaf_counts.max())
+    for lo, hi in ((0, 13), (13, Bl)):
+        scratch = torch.empty(int(lib.rfxc_bucket_scratch_bytes(n, hi - lo)), dtype=torch.uint8,
+                              device=perm.device)
+        _lib.call("rfxc_bucket_trees", _lib.ptr(d.codes_tm), n, Bl, _lib.ptr(d.leaf_base), maxl,
+                  lo, hi, _lib.ptr(p2), _lib.ptr(s2), _lib.ptr(scratch), _lib.ptr(he),
+                  _lib.stream_handle())
+    assert torch.equal(p2, perm) and torch.equal(s2, seg)
+    assert int(he.item()) == int(d.has_empty.item())
