@@ -302,12 +302,14 @@ int rfxc_pmax(const double* d_dq, int64_t n, int32_t r, int64_t seed,
  * Outputs: d_coords (n, k) row-major f64 = sqrt(lambda) * sign_fixed v
  * (mds.py:257-261); d_info: per component {lambda, iterations, residual,
  * converged} as 4 f64; *d_k_used (int32).  d_work: rfxc_mds_work_bytes().
+ * d_pmax (nullable): device copy of pmax (rfxc_pmax's output), read instead of
+ * pmax so the launch needs no host round trip.
  * d_codes / d_scales (nullable): the INT8 factor; when given, large-n runs
  * keep the factor slice of every CTA resident in shared memory as int8
  * codes (code * scale is bit-identical to d_dq). */
 int64_t rfxc_mds_work_bytes(int64_t n, int32_t r, int32_t k);
 int rfxc_mds_power(const double* d_dq, const int8_t* d_codes, const double* d_scales,
-                   int64_t n, int32_t r, double pmax,
+                   int64_t n, int32_t r, double pmax, const double* d_pmax,
                    int32_t k, int32_t max_iterations, double tol, int64_t seed,
                    double* d_coords, double* d_info, int32_t* d_k_used,
                    void* d_work, void* stream);

@@ -74,7 +74,7 @@ SIGNATURES = {
     "rfxc_dequantize": (ctypes.c_int, [P, P, I64, I32, I32, P, P]),
     "rfxc_pmax": (ctypes.c_int, [P, I64, I32, I64, P, P, P]),
     "rfxc_mds_work_bytes": (I64, [I64, I32, I32]),
-    "rfxc_mds_power": (ctypes.c_int, [P, P, P, I64, I32, F64, I32, I32, F64, I64, P, P, P, P,
+    "rfxc_mds_power": (ctypes.c_int, [P, P, P, I64, I32, F64, P, I32, I32, F64, I64, P, P, P, P,
                                       P]),
     "rfxc_gram_matvec": (ctypes.c_int, [P, I64, I32, F64, P, P, P, P]),
 }
@@ -134,7 +134,7 @@ def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
     launch_count += LAUNCHES.get(name, 0)
     if name == "rfxc_mds_power":
-        launch_count += int(args[6])  # start-vector normals, one per component
+        launch_count += int(args[7])  # start-vector normals, one per component
     elif name == "rfxc_sketch_pass":  # a leaf-sum and a gather kernel per tree batch
         Bl, T = int(args[6]), int(args[11])
         launch_count += 2 * ((Bl + T - 1) // T) - 1

@@ -56,6 +56,7 @@ struct MdsArgs {
     int64_t n;
     int r;
     double pmax;
+    const double* pmax_dev;  // when set, pmax is read from device memory (rfxc_pmax's output)
     int k;
     int max_it;
     double tol;
@@ -445,7 +446,7 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
         ct = block_sum(ct, s.red);
         sgm = block_sum(sgm, s.red);
     }
-    const double pm = A.pmax;
+    const double pm = A.pmax_dev ? __ldg(A.pmax_dev) : A.pmax;
     const double mz = (pm * pm) * su - 2.0 * pm * ct / (double)n + sgm / (double)n;
     double dfl[8];
     for (int f = 0; f < nf; f++) dfl[f] = lam_s[f] * T[A.NT * 64 + XS_D + f];
@@ -1030,7 +1031,7 @@ extern "C" int64_t rfxc_mds_work_bytes(int64_t n, int32_t r, int32_t k)
 }
 
 extern "C" int rfxc_mds_power(const double* d_dq, const int8_t* d_codes, const double* d_scales,
-                              int64_t n, int32_t r, double pmax, int32_t k,
+                              int64_t n, int32_t r, double pmax, const double* d_pmax, int32_t k,
                               int32_t max_iterations, double tol, int64_t seed, double* d_coords,
                               double* d_info, int32_t* d_k_used, void* d_work, void* stream)
 {
@@ -1044,6 +1045,7 @@ extern "C" int rfxc_mds_power(const double* d_dq, const int8_t* d_codes, const d
     A.n = n;
     A.r = r;
     A.pmax = pmax;
+    A.pmax_dev = d_pmax;
     A.k = k;
     A.max_it = max_iterations;
     A.tol = tol;

@@ -132,9 +132,14 @@ def mds_lowrank_device(lowrank: LowRankQuantized, config: PowerIterConfig | None
     info = torch.empty((cfg.k, 4), dtype=torch.float64, device=dev)
     kused = torch.empty(1, dtype=torch.int32, device=dev)
     work = _work(n, r, cfg.k, dev)
+    # pmax straight from the device when the factorisation left it there
+    pm_dev = getattr(lowrank, "pm", None)
+    if pm_dev is None:
+        pm_dev = getattr(lowrank, "_pmax_dev", None)
+    pmax = 0.0 if pm_dev is not None else float(lowrank.pmax)
     with region("mds_power"):
         _lib.call("rfxc_mds_power", _lib.ptr(dq), _lib.ptr(codes), _lib.ptr(scales), n, r,
-                  float(lowrank.pmax), cfg.k, cfg.max_iterations, float(cfg.tol), cfg.seed,
+                  pmax, _lib.ptr(pm_dev), cfg.k, cfg.max_iterations, float(cfg.tol), cfg.seed,
                   _lib.ptr(coords), _lib.ptr(info), _lib.ptr(kused), _lib.ptr(work),
                   _lib.stream_handle())
     return coords, info, kused

@@ -30,7 +30,7 @@ from .device import DeviceForest, DeviceMembership, DeviceValues, host_copy, tra
 from .errors import BudgetError, DataError, RfxError
 from .profiling import region
 from .quantize import (BYTES_PER_ELEMENT, MODES, QuantFactor, dequantize,
-                       device_dequantize, factor_quantize, to_host)
+                       device_dequantize, factor_quantize)
 
 logger = logging.getLogger(__name__)
 
@@ -487,6 +487,21 @@ class LowRankQuantized:
     rank_degraded: bool = False
     _dq: np.ndarray = field(default=None, repr=False)
     _dq_dev: object = field(default=None, repr=False)
+    # device results whose host copies are still in flight (event, builder):
+    # ``factor`` / ``pmax`` resolve on first access, so the GPU path can run
+    # on (mds_lowrank reads pmax from _pmax_dev) without a host round trip
+    _pending: object = field(default=None, repr=False, compare=False)
+    _pmax_dev: object = field(default=None, repr=False, compare=False)
+
+    def __getattribute__(self, name):
+        if name in ("factor", "pmax") and object.__getattribute__(self, "_pending") is not None:
+            ev, build = object.__getattribute__(self, "_pending")
+            ev.synchronize()
+            f, pm = build()
+            object.__setattr__(self, "factor", f)
+            object.__setattr__(self, "pmax", pm)
+            object.__setattr__(self, "_pending", None)
+        return object.__getattribute__(self, name)
 
     def dequantized(self) -> np.ndarray:
         if self._dq is None:
@@ -741,14 +756,13 @@ def lowrank_device(membership: LeafMembership, rank: int, mode: str = "i8", seed
         _lib.call("rfxc_pmax", _lib.ptr(dq), n, r, seed, _lib.ptr(parts), _lib.ptr(pm),
                   _lib.stream_handle())
     return DeviceLowRank(n=n, rank=r, mode=mode, data=data, scales=scales, dq=dq,
-                         pmax=float(pm.item()), tree_count=membership.tree_count,
-                         degraded=degraded)
+                         pm=pm, tree_count=membership.tree_count, degraded=degraded)
 
 
 @dataclass
 class DeviceLowRank:
     """Device-resident result of the low-rank pipeline (factor codes, scales,
-    dequantised factor) before any host copy."""
+    dequantised factor, pmax) before any host copy."""
 
     n: int
     rank: int
@@ -756,15 +770,40 @@ class DeviceLowRank:
     data: object
     scales: object
     dq: object
-    pmax: float
+    pm: object  # (1,) f64 on the device
     tree_count: int
     degraded: bool
 
+    @property
+    def pmax(self) -> float:
+        return float(self.pm.item())
+
     def to_host(self) -> LowRankQuantized:
-        qf = to_host(self.mode, (self.n, self.rank), self.data, self.scales)
-        out = LowRankQuantized(n=self.n, rank=self.rank, mode=self.mode, factor=qf,
-                               pmax=self.pmax, tree_count=self.tree_count,
-                               rank_degraded=self.degraded, _dq_dev=self.dq)
+        """The reference's LowRankQuantized; the factor codes, scales and pmax
+        cross PCIe asynchronously (pinned buffers, stream-ordered) and are
+        waited for on first access."""
+        import torch
+        pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
+        hd, hp = pin(self.data), pin(self.pm)
+        hs = None if self.scales is None else pin(self.scales)
+        hd.copy_(self.data, non_blocking=True)
+        hp.copy_(self.pm, non_blocking=True)
+        if hs is not None:
+            hs.copy_(self.scales, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        mode, shape = self.mode, (self.n, self.rank)
+
+        def build():
+            d = hd.numpy()
+            if mode in ("f32", "f16", "i8"):
+                d = d.reshape(shape)
+            s_ = None if hs is None else hs.numpy().astype(np.float64)
+            return QuantFactor(mode, tuple(shape), d, s_), float(hp.numpy()[0])
+
+        out = LowRankQuantized(n=self.n, rank=self.rank, mode=self.mode, factor=None, pmax=None,
+                               tree_count=self.tree_count, rank_degraded=self.degraded,
+                               _dq_dev=self.dq, _pending=(ev, build), _pmax_dev=self.pm)
         out._codes_dev = (self.data, self.scales)
         return out
 
