@@ -401,26 +401,39 @@ def traverse(dforest: DeviceForest, dvalues: DeviceValues):
     cur = torch.cuda.current_stream()
     f32_rows = dvalues.rows_ready if layout == _lib.NODES_F32 else []
     done = []  # (c0, c1, event after the chunk's codes)
+
+    def walk(c0, c1, lo, hi):
+        _lib.call("rfxc_leaf_codes_rows", _lib.ptr(dforest._nodes), _lib.ptr(dforest.node_off),
+                  layout, dvalues.p, c0, c1, _lib.ptr(vals), n, lo, hi, _lib.ptr(tm[c0:c1]),
+                  _lib.stream_handle())
+
+    def mark(c0, c1):
+        cev = torch.cuda.Event()
+        cev.record(cur)
+        done.append((c0, c1, cev))
+
+    chunks = list(dforest.chunks)
     with region("leaf_codes"):
-        for j, (c0, c1, ev) in enumerate(dforest.chunks):  # after its node records arrived
+        rest = chunks
+        if len(f32_rows) > 1:
+            # values arrived in sample blocks: the first two tree chunks walk
+            # each block as soon as it is there (block-major), so the
+            # traversal starts after ~1/4 of the bytes
+            early, rest = chunks[:2], chunks[2:]
+            blocks = list(zip([0] + [h for h, _ in f32_rows], f32_rows))
+            for bi, (lo, (hi, e)) in enumerate(blocks):
+                cur.wait_event(e)
+                for c0, c1, ev in early:
+                    cur.wait_event(ev)
+                    walk(c0, c1, lo, hi)
+                    if bi == len(blocks) - 1:
+                        mark(c0, c1)
+        if rest and dvalues.ready is not None:
+            cur.wait_event(dvalues.ready)
+        for c0, c1, ev in rest:  # after its node records arrived
             cur.wait_event(ev)
-            # the first chunk walks each sample block as soon as its rows
-            # have arrived; later chunks need every row
-            blocks = [(lo, hi, e) for (lo, (hi, e)) in zip([0] + [h for h, _ in f32_rows],
-                                                            f32_rows)] if j == 0 else []
-            if not blocks:
-                if dvalues.ready is not None:
-                    cur.wait_event(dvalues.ready)
-                blocks = [(0, n, None)]
-            for lo, hi, e in blocks:
-                if e is not None:
-                    cur.wait_event(e)
-                _lib.call("rfxc_leaf_codes_rows", _lib.ptr(dforest._nodes),
-                          _lib.ptr(dforest.node_off), layout, dvalues.p, c0, c1, _lib.ptr(vals),
-                          n, lo, hi, _lib.ptr(tm[c0:c1]), _lib.stream_handle())
-            cev = torch.cuda.Event()
-            cev.record(cur)
-            done.append((c0, c1, cev))
+            walk(c0, c1, 0, n)
+            mark(c0, c1)
     nb = torch.empty((n, Bl), dtype=torch.int32, device=dev)
     _lib.call("rfxc_transpose_i32", _lib.ptr(tm), Bl, n, _lib.ptr(nb), _lib.stream_handle())
     return nb, tm, done

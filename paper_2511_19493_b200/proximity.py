@@ -160,17 +160,20 @@ def leaf_membership(forest, dataset, trees: tuple | None = None) -> LeafMembersh
     dvals = DeviceValues(dataset.values, defer=True)
     layout = None if dvals.exact_f32 else _lib.NODES_F64
     dforest = DeviceForest(forest, *local, layout=layout, defer=True)
-    # PCIe order: the first half of the samples, the first (small) tree chunk,
-    # the other samples, the other chunks — the first traversal launch then
-    # waits for ~1/4 of the bytes instead of all values + a full chunk
+    # PCIe order: the first half of the samples, the first two tree chunks
+    # (the first one small), the other samples, the other chunks — traverse()
+    # walks the first two chunks sample block by sample block, so the first
+    # launch waits for ~1/4 of the bytes instead of all values + a full chunk
     n = dvals.n
     split = (n // 2) // 128 * 128 if dvals.exact_f32 and n >= 256 else 0
     if split:
         dvals.upload_rows(0, split)
-    dforest.upload_chunk(0)
+    first = min(2, len(dforest._spans)) if split else 1
+    for j in range(first):
+        dforest.upload_chunk(j)
     if dvals.exact_f32:
         dvals.upload_rows(split, n)
-    for j in range(1, len(dforest._spans)):
+    for j in range(first, len(dforest._spans)):
         dforest.upload_chunk(j)
     nb, tm, chunks = traverse(dforest, dvals)
     dev = DeviceMembership(nb, tm, dforest.leaf_counts, lo, hi, B, chunks)
