@@ -107,3 +107,22 @@ def test_deterministic():
     a = M.mds_lowrank(ref_lowrank(g, 178), M.PowerIterConfig(seed=9))
     b = M.mds_lowrank(ref_lowrank(g, 178), M.PowerIterConfig(seed=9))
     assert np.array_equal(a.coordinates, b.coordinates)
+
+
+def test_int8_resident_slices_large_n(orc):
+    """n = 150k, r = 32: the f64 factor slice no longer fits shared memory,
+    so every CTA keeps int8 codes x scales (QS_I8 layout); five power
+    iterations of three components against the oracle restatement."""
+    rng = np.random.default_rng(11)
+    n, r = 150_000, 32
+    data = rng.integers(-127, 128, size=(n, r)).astype(np.int8)
+    scales = rng.uniform(0.5e-3, 2e-3, r)
+    Q = data.astype(np.float64) * scales[None, :]
+    pmax = float(np.einsum("ij,ij->i", Q, Q).max())
+    lr = P.LowRankQuantized(n=n, rank=r, mode="i8", factor=QuantFactor("i8", (n, r), data, scales),
+                            pmax=pmax, tree_count=100)
+    emb = M.mds_lowrank(lr, M.PowerIterConfig(seed=0, max_iterations=5, tol=1e-30, k=3))
+    coords, eig, its, *_ = orc.mds_lowrank(Q, pmax, max_iterations=5, tol=1e-30, k=3, seed=0)
+    assert np.all(emb.iterations == its)
+    np.testing.assert_allclose(emb.eigenvalues, eig, rtol=1e-9)
+    np.testing.assert_allclose(emb.coordinates, coords, rtol=1e-6, atol=1e-9 * np.abs(coords).max())
