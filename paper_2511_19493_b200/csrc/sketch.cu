@@ -543,7 +543,7 @@ matmul_small_kernel(const double* __restrict__ Y, int64_t n, int ka, const doubl
 // in tree b0+t (one coalesced segment of the (n, B) membership), the T
 // leaf-sum rows are gathered as float4 lanes and summed in f32, and the sum
 // is added to Y in f64 (scaled by 1/B in the last batch).
-constexpr int SKP_SAMPLES = 24;  // samples per phase-B item
+constexpr int SKP_SAMPLES = 24;  // max samples per phase-B item (A.spw: one wave of resident warps)
 constexpr int SKP_RMAX = 4;      // row slots per warp (lane groups of k4 lanes)
 constexpr int SKP_MAX_T = 32;
 
@@ -590,6 +590,7 @@ struct SkpArgs {
     unsigned* ctr;             // 2 x (nbatch + 1)
     const int32_t* item_leaf;  // nbatch x ipb
     int64_t n, s_rows, ipb, item;
+    int spw;                   // phase-B samples per warp
     int Bl, k, ld, T, nbatch;
     int nbuf;                  // leaf-sum buffers (1: A(e), B(e) on one stream)
     double scale;
@@ -921,7 +922,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
     skp_emit(A, cy[0], cy[1], cy[2], cy[3], cleaf, kind, it, pos0, g0, Sb, lane, slot == 0);
 }
 
-// Phase B item: samples [i0, i0 + SKP_SAMPLES) against batch e's leaf sums.
+// Phase B item: samples [i0, i0 + A.spw) against batch e's leaf sums.
 // Slot s takes every R-th sample; its lanes gather the nT leaf-sum rows of
 // that sample (coalesced, SKP_UB in flight), sum them in f32 and add the sum
 // to Y in f64 (scaled by 1/B in the last batch).
@@ -937,7 +938,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
     const int slot = lane / k4, c4 = lane - slot * k4;
     const bool on = slot < R;
     const bool first = e == 0, last = e == A.nbatch - 1;
-    const int64_t i0 = it * SKP_SAMPLES, i1 = min64(i0 + SKP_SAMPLES, A.n);
+    const int64_t i0 = it * A.spw, i1 = min64(i0 + A.spw, A.n);
     const int32_t lb = lane < nT ? (int32_t)(A.leaf_base[b0 + lane] - g0) : 0;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     const int* rb = reinterpret_cast<const int*>(rbuf) + (on ? slot : 0) * SKP_SLOT;
@@ -1021,7 +1022,7 @@ __global__ void __launch_bounds__(256, PH == 0 ? SKP_MINB_A : 4) sketch_phase_ke
         const int64_t nA = ((int64_t)(b1 - b0) * A.n + A.item - 1) / A.item;
         if (q < nA) skp_phase_a<K4>(A, e, q, scratch, lane);
     } else {
-        const int64_t nB = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
+        const int64_t nB = (A.n + A.spw - 1) / A.spw;
         if (q < nB) skp_phase_b<K4>(A, e, q, scratch, lane);
     }
 }
@@ -1284,7 +1285,7 @@ static void launch_phase(const SkpArgs& A, int e, cudaStream_t s)
         const int b0 = e * A.T, b1 = std::min(A.Bl, b0 + A.T);
         items = ((int64_t)(b1 - b0) * A.n + A.item - 1) / A.item;
     } else {
-        items = (A.n + SKP_SAMPLES - 1) / SKP_SAMPLES;
+        items = (A.n + A.spw - 1) / A.spw;
     }
     if (A.ld == 40)  // k = r + 8 for the default rank 32
         sketch_phase_kernel<PH, 10><<<(unsigned)ceil_div(items, 8), 256, smem, s>>>(A, e);
@@ -1361,6 +1362,10 @@ extern "C" int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg,
     A.n = n;
     A.s_rows = s_rows;
     A.item = item;
+    {   // phase B: all items in one wave of resident warps (4 CTAs x 8 warps per SM)
+        const int64_t warps = (int64_t)sm_count() * 4 * 8;
+        A.spw = (int)std::min<int64_t>(SKP_SAMPLES, std::max<int64_t>(1, (n + warps - 1) / warps));
+    }
     A.ipb = skp_items_per_batch(n, T, item);
     A.Bl = Bl;
     A.k = k;
