@@ -829,8 +829,7 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
             }
             cur = he ? skp_leaf_at(A.seg, g0, gN, q0 + p) : cur + 1;
             inside = true;
-            acc = z4;
-        };
+        };  // the caller restarts acc with the row at p
         static_assert(SKP_UA == 4, "index loads are uint4");
         if (P1 - (P0 + 32 * (int64_t)s0) >= 32 * R) {
             // every slot has 32 positions: no predicates (lanes past the last
@@ -849,14 +848,10 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
                     f4add(acc, x2);
                     f4add(acc, x3);
                 } else {
-                    if (f4 & 1u) flush(p0);
-                    f4add(acc, x0);
-                    if (f4 & 2u) flush(p0 + 1);
-                    f4add(acc, x1);
-                    if (f4 & 4u) flush(p0 + 2);
-                    f4add(acc, x2);
-                    if (f4 & 8u) flush(p0 + 3);
-                    f4add(acc, x3);
+                    if (f4 & 1u) { flush(p0); acc = x0; } else { f4add(acc, x0); }
+                    if (f4 & 2u) { flush(p0 + 1); acc = x1; } else { f4add(acc, x1); }
+                    if (f4 & 4u) { flush(p0 + 2); acc = x2; } else { f4add(acc, x2); }
+                    if (f4 & 8u) { flush(p0 + 3); acc = x3; } else { f4add(acc, x3); }
                 }
             }
         } else {
@@ -869,8 +864,12 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
                     x[u] = (on && p0 + u < m) ? __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ixs[u] << 4))) : z4;
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    if ((fsx >> (p0 + u)) & 1u) flush(p0 + u);
-                    f4add(acc, x[u]);
+                    if ((fsx >> (p0 + u)) & 1u) {
+                        flush(p0 + u);
+                        acc = x[u];
+                    } else {
+                        f4add(acc, x[u]);
+                    }
                 }
             }
         }
