@@ -17,7 +17,6 @@ from .errors import BudgetError, DataError, RfxError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 BUILD_DIR = os.path.join(_HERE, "_build")
 LIB_PATH = os.path.join(BUILD_DIR, "librfxc.so")
-TRAIN_LIB_PATH = os.path.join(BUILD_DIR, "librfx_train.so")
 
 RFXC_OK, RFXC_EDATA, RFXC_EBUDGET, RFXC_ERUNTIME, RFXC_ECUDA = range(5)
 NODES_F32, NODES_F64 = 0, 1
@@ -51,6 +50,9 @@ SIGNATURES = {
     "rfxc_bucket": (ctypes.c_int, [P, I64, I32, P, I32, P, P, P, P, P]),
     "rfxc_bucket_trees": (ctypes.c_int, [P, I64, I32, P, I32, I32, I32, P, P, P, P, P]),
     "rfxc_pair_counts": (ctypes.c_int, [P, I64, I32, I64, I64, I32, P, P]),
+    "rfxc_pair_counts_leaf": (ctypes.c_int, [P, P, P, P, P, I64, I32, I64, I64, I32, P, P]),
+    "rfxc_perm_positions": (ctypes.c_int, [P, I64, I32, P, P]),
+    "rfxc_same_leaf_pairs": (ctypes.c_int, [P, I64, P, P]),
     "rfxc_triblock_count": (ctypes.c_int, [P, I64, I32, I64, I64, F64, P, P]),
     "rfxc_triblock_emit": (ctypes.c_int, [P, I64, I32, I64, I64, F64, P, P, P, P, P, P, P,
                                           P]),

@@ -16,6 +16,8 @@
 // division, bit-identical to counts / float(B)), or the TriBlock row block.
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace rfxc {
 
 constexpr int PT = 128;     // tile edge
@@ -94,6 +96,134 @@ pair_tile_kernel(const int32_t* __restrict__ codes, int64_t n, int32_t B, int64_
             else
                 reinterpret_cast<int32_t*>(out)[(i - row_lo) * n + j] = acc[a][c];
         }
+    }
+}
+
+// ------------------------------------------------- leaf-segmented counts
+// The reference's own formulation (accumulate_pair_counts, _kernels.py:
+// 491-510): per tree, every same-leaf pair (i, j) of the bucketed samples
+// adds one.  Here it is row-stationary so that the output is written once,
+// coalesced: a CTA owns output row i (a window of its columns at a time) as
+// packed 16-bit counters in shared memory; for every tree a warp reads the
+// members that follow i in its leaf's run of the K2 bucket (one coalesced
+// 32-entry read of perm from pos_nb[i, b] + 1 up to the next first-member
+// flag), and bumps their counters with shared-memory atomics.  Work is
+// n*B warp-steps + (same-leaf pairs)/32 instead of n^2*B/2 compares, so at
+// the configs' leaf sizes (0.8 % of pairs share a leaf per tree at 50k) the
+// kernel is bound by writing the triangle, not by the counting.  Integer
+// sums: bit-exact and order-independent.
+constexpr int SEG_THREADS = 512;
+constexpr int SEG_UNROLL = 4;
+
+// pos_tm[b * n + sample] = absolute index of the sample in perm (tree b).
+__global__ void perm_inverse_kernel(const uint32_t* __restrict__ perm, int64_t total, int64_t n,
+                                    uint32_t* __restrict__ pos_tm)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += stride) {
+        const int64_t b = e / n;
+        const uint32_t s = __ldg(perm + e) & ~RFXC_PERM_FIRST;
+        pos_tm[b * n + s] = (uint32_t)e;
+    }
+}
+
+// sum over leaves of s (s - 1) / 2 from the run starts (integer, exact).
+__global__ void same_leaf_pairs_kernel(const int64_t* __restrict__ seg, int64_t leaves,
+                                       unsigned long long* __restrict__ out)
+{
+    unsigned long long acc = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < leaves; g += stride) {
+        const unsigned long long s = (unsigned long long)(seg[g + 1] - seg[g]);
+        acc += s * (s - (s > 0)) / 2;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+template <int LAYOUT>
+__global__ void __launch_bounds__(SEG_THREADS, 2)
+pair_seg_kernel(const uint32_t* __restrict__ pos_nb, const uint32_t* __restrict__ perm,
+                const int32_t* __restrict__ codes_nb, const int64_t* __restrict__ seg,
+                const int64_t* __restrict__ leaf_base, int64_t n, int32_t B, int64_t row_lo,
+                int64_t row_hi, int64_t win, void* __restrict__ out)
+{
+    extern __shared__ uint32_t cnt[];  // win/2 words: counters of columns [c0, c0 + win)
+    constexpr int NW = SEG_THREADS / 32;
+    __shared__ int32_t s_end[NW][33];   // per warp: exclusive/inclusive entry prefix of 32 trees
+    __shared__ int64_t s_base[NW][32];  // perm index of entry 0 of each tree's members after i
+    const int64_t i = row_lo + blockIdx.x;
+    if (i >= row_hi) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t rbase = row_start(i, n) - row_start(row_lo, n) - i - 1;
+    const double dB = (double)B;
+    for (int64_t c0 = i + 1; c0 < n; c0 += win) {
+        const int64_t c1 = min64(n, c0 + win);
+        const int64_t words = (c1 - c0 + 1) >> 1;
+        for (int64_t w = tid; w < words; w += SEG_THREADS) cnt[w] = 0u;
+        __syncthreads();
+        for (int b0 = warp * 32; b0 < B; b0 += NW * 32) {
+            // lane = tree b0 + lane: members of i's leaf that follow i in the
+            // run (samples > i, ascending), i.e. perm (p, end)
+            const int b = b0 + lane;
+            int32_t m = 0;
+            int64_t base = 0;
+            if (b < B) {
+                const int64_t p = (int64_t)__ldg(pos_nb + i * B + b);
+                const int64_t g = __ldg(leaf_base + b) + __ldg(codes_nb + i * B + b);
+                m = (int32_t)(__ldg(seg + g + 1) - p - 1);
+                base = p + 1;
+            }
+            int32_t incl = m;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            s_end[warp][lane + 1] = incl;
+            if (lane == 0) s_end[warp][0] = 0;
+            s_base[warp][lane] = base - (incl - m);  // perm index = s_base[t] + entry
+            __syncwarp();
+            // flat walk over the group's entries, one per lane: every lane busy
+            // whatever the run lengths; t = the tree of this lane's entry
+            int t = 0;
+            for (int32_t e0 = 0; e0 < total; e0 += 32 * SEG_UNROLL) {
+                uint32_t v[SEG_UNROLL];
+#pragma unroll
+                for (int u = 0; u < SEG_UNROLL; u++) {
+                    const int32_t e = e0 + u * 32 + lane;
+                    v[u] = 0xffffffffu;
+                    if (e < total) {
+                        while (s_end[warp][t + 1] <= e) t++;
+                        v[u] = __ldg(perm + s_base[warp][t] + e);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < SEG_UNROLL; u++) {
+                    if (v[u] == 0xffffffffu) continue;
+                    const int64_t j = (int64_t)(v[u] & ~RFXC_PERM_FIRST);
+                    if (j >= c0 && j < c1) {
+                        const int64_t o = j - c0;
+                        atomicAdd(cnt + (o >> 1), 1u << ((o & 1) << 4));
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        for (int64_t j = c0 + tid; j < c1; j += SEG_THREADS) {
+            const int64_t o = j - c0;
+            const int32_t c = (int32_t)((cnt[o >> 1] >> ((o & 1) << 4)) & 0xffffu);
+            if (LAYOUT == RFXC_UPPER_I32)
+                reinterpret_cast<int32_t*>(out)[rbase + j] = c;
+            else if (LAYOUT == RFXC_UPPER_F64)
+                reinterpret_cast<double*>(out)[rbase + j] = (double)c / dB;
+            else
+                reinterpret_cast<int32_t*>(out)[(i - row_lo) * n + j] = c;
+        }
+        __syncthreads();
     }
 }
 
@@ -246,6 +376,75 @@ extern "C" int rfxc_pair_counts(const int32_t* d_codes_nb, int64_t n, int32_t B,
         return fail(RFXC_EDATA, "pair_counts: unknown layout %d", layout);
     }
     return check_launch("pair_counts");
+}
+
+extern "C" int rfxc_perm_positions(const uint32_t* d_perm, int64_t n, int32_t Bl,
+                                   uint32_t* d_pos_tm, void* stream)
+{
+    const int64_t total = n * (int64_t)Bl;
+    if (n < 1 || Bl < 1 || total >= ((int64_t)1 << 32))
+        return fail(RFXC_EDATA, "perm_positions: n*Bl = %lld outside [1, 2^32)", (long long)total);
+    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 16);
+    perm_inverse_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_perm, total, n, d_pos_tm);
+    return check_launch("perm_positions");
+}
+
+extern "C" int rfxc_same_leaf_pairs(const int64_t* d_seg, int64_t leaves, uint64_t* d_out,
+                                    void* stream)
+{
+    cudaStream_t st = as_stream(stream);
+    cudaError_t e = cudaMemsetAsync(d_out, 0, sizeof(uint64_t), st);
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "memset: %s", cudaGetErrorString(e));
+    if (leaves <= 0) return RFXC_OK;
+    const int grid = (int)std::min<int64_t>(ceil_div(leaves, 256), (int64_t)sm_count() * 8);
+    same_leaf_pairs_kernel<<<grid, 256, 0, st>>>(d_seg, leaves,
+                                                 reinterpret_cast<unsigned long long*>(d_out));
+    return check_launch("same_leaf_pairs");
+}
+
+template <int LAYOUT>
+static int launch_seg(const uint32_t* pos_nb, const uint32_t* perm, const int32_t* codes_nb,
+                      const int64_t* seg, const int64_t* leaf_base, int64_t n, int32_t B,
+                      int64_t row_lo, int64_t row_hi, int64_t win, void* out, cudaStream_t st)
+{
+    const size_t smem = (size_t)((win + 1) / 2) * 4;
+    cudaError_t e = cudaFuncSetAttribute(pair_seg_kernel<LAYOUT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "pair_seg smem: %s", cudaGetErrorString(e));
+    pair_seg_kernel<LAYOUT><<<(unsigned)(row_hi - row_lo), SEG_THREADS, smem, st>>>(
+        pos_nb, perm, codes_nb, seg, leaf_base, n, B, row_lo, row_hi, win, out);
+    return check_launch("pair_counts_leaf");
+}
+
+extern "C" int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const uint32_t* d_perm,
+                                     const int32_t* d_codes_nb, const int64_t* d_seg,
+                                     const int64_t* d_leaf_base, int64_t n, int32_t B,
+                                     int64_t row_lo, int64_t row_hi, int32_t layout, void* d_out,
+                                     void* stream)
+{
+    if (n < 2 || B < 1 || row_lo < 0 || row_hi > n || row_lo >= row_hi)
+        return fail(RFXC_EDATA, "pair_counts_leaf: bad shape n=%lld rows=[%lld,%lld)",
+                    (long long)n, (long long)row_lo, (long long)row_hi);
+    if (B > 65535) return fail(RFXC_EDATA, "pair_counts_leaf: B=%d > 65535 (16-bit counters)", B);
+    if (row_hi - row_lo > 0x7fffffffLL) return fail(RFXC_EDATA, "pair_counts_leaf: rows");
+    cudaStream_t st = as_stream(stream);
+    // counters of up to 48k columns per pass: two CTAs of 512 threads per SM
+    int64_t cap = 48 * 1024;
+    if (const char* w = getenv("RFXC_PAIRS_WINDOW")) cap = std::max<int64_t>(2, atoll(w));  // tests
+    const int64_t win = std::max<int64_t>(1, std::min<int64_t>(n - 1 - row_lo, cap));
+    switch (layout) {
+    case RFXC_UPPER_I32:
+        return launch_seg<RFXC_UPPER_I32>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base, n, B, row_lo, row_hi, win, d_out, st);
+    case RFXC_UPPER_F64:
+        return launch_seg<RFXC_UPPER_F64>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base, n, B, row_lo, row_hi, win, d_out, st);
+    case RFXC_BLOCK_I32: {
+        cudaError_t e = cudaMemsetAsync(d_out, 0, (size_t)(row_hi - row_lo) * n * 4, st);
+        if (e != cudaSuccess) return fail(RFXC_ECUDA, "memset: %s", cudaGetErrorString(e));
+        return launch_seg<RFXC_BLOCK_I32>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base, n, B, row_lo, row_hi, win, d_out, st);
+    }
+    default:
+        return fail(RFXC_EDATA, "pair_counts_leaf: unknown layout %d", layout);
+    }
 }
 
 extern "C" int rfxc_triblock_count(const int32_t* d_counts_upper, int64_t n, int32_t B,

@@ -334,6 +334,8 @@ class DeviceMembership:
         self._perm = None
         self._seg = None
         self._has_empty = None
+        self._pos = None
+        self._pairs = None
 
     @property
     def Bl(self) -> int:
@@ -364,6 +366,33 @@ class DeviceMembership:
                           _lib.stream_handle())
             self._perm, self._seg, self._has_empty = perm, seg, has_empty
         return self._perm, self._seg
+
+    def positions(self):
+        """(n, Bl) uint32: index of sample i in perm for tree b (the start of
+        i's walk in the leaf-segmented pair counts).  Built once from K2."""
+        torch = _torch()
+        if self._pos is None:
+            perm, _ = self.buckets()
+            tm = torch.empty((self.Bl, self.n), dtype=torch.int32, device=perm.device)
+            nb = torch.empty((self.n, self.Bl), dtype=torch.int32, device=perm.device)
+            with region("positions"):
+                _lib.call("rfxc_perm_positions", _lib.ptr(perm), self.n, self.Bl, _lib.ptr(tm),
+                          _lib.stream_handle())
+                _lib.call("rfxc_transpose_i32", _lib.ptr(tm), self.Bl, self.n, _lib.ptr(nb),
+                          _lib.stream_handle())
+            self._pos = nb
+        return self._pos
+
+    def same_leaf_pairs(self) -> int:
+        """Sum over the local trees' leaves of s(s-1)/2 (exact integer)."""
+        torch = _torch()
+        if self._pairs is None:
+            _, seg = self.buckets()
+            out = torch.empty(1, dtype=torch.int64, device=seg.device)
+            _lib.call("rfxc_same_leaf_pairs", _lib.ptr(seg), self.total_leaves, _lib.ptr(out),
+                      _lib.stream_handle())
+            self._pairs = int(out.item())
+        return self._pairs
 
     @property
     def has_empty(self):

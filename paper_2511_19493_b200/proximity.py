@@ -270,9 +270,36 @@ def pair_counts_device(membership: LeafMembership, layout: int, row_lo: int = 0,
     _device_budget(numel * (8 if dt == torch.float64 else 4), "pair counts", n, B)
     out = torch.empty(max(numel, 1), dtype=dt, device=d.codes_nb.device)
     if n >= 2 and row_hi > row_lo:
-        _lib.call("rfxc_pair_counts", _lib.ptr(d.codes_nb), n, B, row_lo, row_hi, layout,
-                  _lib.ptr(out), _lib.stream_handle())
+        if pair_kernel(d) == "leaf":
+            pos, (perm, seg) = d.positions(), d.buckets()
+            with region("pair_counts"):
+                _lib.call("rfxc_pair_counts_leaf", _lib.ptr(pos), _lib.ptr(perm),
+                          _lib.ptr(d.codes_nb), _lib.ptr(seg), _lib.ptr(d.leaf_base), n, B,
+                          row_lo, row_hi, layout, _lib.ptr(out), _lib.stream_handle())
+        else:
+            with region("pair_counts"):
+                _lib.call("rfxc_pair_counts", _lib.ptr(d.codes_nb), n, B, row_lo, row_hi, layout,
+                          _lib.ptr(out), _lib.stream_handle())
     return out[:numel]
+
+
+# The leaf-segmented kernel costs ~ n*B + (same-leaf pairs)/32 warp steps; the
+# tile kernel n^2*B/2 compares whatever the leaves.  Measured crossover: the
+# segmented kernel wins while same-leaf pairs are below this share of all
+# (pair, tree) units (fully grown trees: well under 1 %).
+LEAF_KERNEL_MAX_SHARE = 0.2
+
+
+def pair_kernel(d) -> str:
+    """'leaf' (K2-bucket walk, the reference's per-leaf formulation) or
+    'tile' (compare tiles); RFX_PAIRS_KERNEL=leaf|tile forces one."""
+    forced = os.environ.get("RFX_PAIRS_KERNEL")
+    if forced in ("leaf", "tile"):
+        return forced
+    if d.B > 65535 or d.n * d.Bl >= (1 << 32):
+        return "tile"
+    units = d.n * (d.n - 1) // 2 * d.Bl
+    return "leaf" if d.same_leaf_pairs() <= LEAF_KERNEL_MAX_SHARE * units else "tile"
 
 
 def full_proximity(membership: LeafMembership,

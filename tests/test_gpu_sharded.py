@@ -35,7 +35,8 @@ def _rank(rank, world, port, out):
         from paper_2511_19493_b200 import distributed as D
         from paper_2511_19493_b200 import proximity as P
         from paper_2511_19493_b200.dataset import from_arrays, make_synthetic
-        from paper_2511_19493_b200.forest import TrainConfig, train
+        from oracle.trainer import train
+        from paper_2511_19493_b200.forest import TrainConfig
         X, y = make_synthetic(3000, 20, seed=2)
         ds = from_arrays(X, y)
         forest = train(ds, TrainConfig(ntree=24, iseed=3))

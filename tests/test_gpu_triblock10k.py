@@ -21,7 +21,8 @@ def tri10k(built):
     from paper_2511_19493_b200 import _lib
     from paper_2511_19493_b200 import proximity as P
     from paper_2511_19493_b200.dataset import from_arrays, make_synthetic
-    from paper_2511_19493_b200.forest import TrainConfig, train
+    from oracle.trainer import train
+    from paper_2511_19493_b200.forest import TrainConfig
     X, y = make_synthetic(10_000, 50, seed=0)
     ds = from_arrays(X, y)
     forest = train(ds, TrainConfig(ntree=500, iseed=1), nthreads=os.cpu_count() or 1)

