@@ -182,7 +182,7 @@ int rfxc_pair_counts(const int32_t* d_codes_nb, int64_t n, int32_t B,
  * (rfxc_perm_positions, then rfxc_transpose_i32); d_codes_nb / d_seg /
  * d_leaf_base as for the sketch give the end of i's run.  Work ~ n*B + same-leaf
  * pairs instead of n^2*B/2; the host picks it when the same-leaf pairs
- * (rfxc_same_leaf_pairs) are a small fraction of n(n-1)/2*B.  B <= 65535.
+ * (rfxc_same_leaf_pairs) are a small fraction of n(n-1)/2*B.  B <= 4096.
  * Same layouts and output as rfxc_pair_counts. */
 int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const uint32_t* d_perm,
                           const int32_t* d_codes_nb, const int64_t* d_seg,

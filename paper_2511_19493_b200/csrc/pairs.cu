@@ -113,7 +113,8 @@ pair_tile_kernel(const int32_t* __restrict__ codes, int64_t n, int32_t B, int64_
 // kernel is bound by writing the triangle, not by the counting.  Integer
 // sums: bit-exact and order-independent.
 constexpr int SEG_THREADS = 512;
-constexpr int SEG_UNROLL = 4;
+constexpr int SEG_UNROLL = 8;
+constexpr int SEG_QUOT_MAX = 4096;
 
 // pos_tm[b * n + sample] = absolute index of the sample in perm (tree b).
 __global__ void perm_inverse_kernel(const uint32_t* __restrict__ perm, int64_t total, int64_t n,
@@ -142,6 +143,27 @@ __global__ void same_leaf_pairs_kernel(const int64_t* __restrict__ seg, int64_t 
     if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
+// Dynamic shared memory of pair_seg_kernel: counters (win/2 words, padded to
+// 8 bytes) | quotient table (B + 1 doubles, f64 layout, B <= SEG_QUOT_MAX) |
+// entry prefix over the trees (B + 1 int32) | run base per tree (B uint32).
+__host__ __device__ __forceinline__ int64_t seg_cnt_words(int64_t win)
+{
+    return (((win + 1) / 2) + 1) & ~(int64_t)1;
+}
+
+template <int LAYOUT>
+__host__ __device__ __forceinline__ bool seg_has_quot(int32_t B)
+{
+    return LAYOUT == RFXC_UPPER_F64 && B <= SEG_QUOT_MAX;
+}
+
+template <int LAYOUT>
+__host__ __device__ __forceinline__ int64_t seg_smem_bytes(int64_t win, int32_t B)
+{
+    return seg_cnt_words(win) * 4 + (seg_has_quot<LAYOUT>(B) ? (int64_t)(B + 1) * 8 : 0) +
+           (int64_t)(2 * B + 2) * 4;
+}
+
 template <int LAYOUT>
 __global__ void __launch_bounds__(SEG_THREADS, 2)
 pair_seg_kernel(const uint32_t* __restrict__ pos_nb, const uint32_t* __restrict__ perm,
@@ -149,79 +171,112 @@ pair_seg_kernel(const uint32_t* __restrict__ pos_nb, const uint32_t* __restrict_
                 const int64_t* __restrict__ leaf_base, int64_t n, int32_t B, int64_t row_lo,
                 int64_t row_hi, int64_t win, void* __restrict__ out)
 {
-    extern __shared__ uint32_t cnt[];  // win/2 words: counters of columns [c0, c0 + win)
+    extern __shared__ __align__(16) uint32_t cnt[];
     constexpr int NW = SEG_THREADS / 32;
-    __shared__ int32_t s_end[NW][33];   // per warp: exclusive/inclusive entry prefix of 32 trees
-    __shared__ int64_t s_base[NW][32];  // perm index of entry 0 of each tree's members after i
+    __shared__ int32_t s_wsum[NW];
     const int64_t i = row_lo + blockIdx.x;
     if (i >= row_hi) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t rbase = row_start(i, n) - row_start(row_lo, n) - i - 1;
     const double dB = (double)B;
+    double* quot = reinterpret_cast<double*>(cnt + seg_cnt_words(win));
+    int32_t* s_end = reinterpret_cast<int32_t*>(quot + (seg_has_quot<LAYOUT>(B) ? B + 1 : 0));
+    uint32_t* s_base = reinterpret_cast<uint32_t*>(s_end + B + 1);
+    // f64 layout: the B + 1 possible quotients c / B (each one IEEE
+    // division), so the epilogue is a table lookup
+    if (seg_has_quot<LAYOUT>(B))
+        for (int c = tid; c <= B; c += SEG_THREADS) quot[c] = (double)c / dB;
+
+    // Tree b: the members of i's leaf that follow i in its run of perm
+    // (samples > i, ascending) — m_b of them from perm index p_b + 1.  Thread
+    // tid owns trees [tid*per, (tid+1)*per); a block scan turns the m_b into
+    // the flat entry space [0, T) that the warps then split evenly.
+    const int per = (B + SEG_THREADS - 1) / SEG_THREADS;
+    const int bl = min(B, tid * per), bh = min(B, bl + per);
+    int32_t mine = 0;
+    for (int b = bl; b < bh; b++) {
+        const uint32_t p = __ldg(pos_nb + i * B + b);
+        const int64_t g = __ldg(leaf_base + b) + __ldg(codes_nb + i * B + b);
+        const int32_t m = (int32_t)(__ldg(seg + g + 1) - (int64_t)p - 1);
+        s_end[b + 1] = m;  // temporarily m_b
+        s_base[b] = p + 1u;
+        mine += m;
+    }
+    int32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    int32_t before = incl - mine;
+    for (int w = 0; w < warp; w++) before += s_wsum[w];
+    for (int b = bl; b < bh; b++) {  // m_b -> inclusive prefix; base - exclusive prefix
+        const int32_t m = s_end[b + 1];
+        s_base[b] -= (uint32_t)before;  // mod 2^32: + flat entry = perm index
+        before += m;
+        s_end[b + 1] = before;
+    }
+    if (tid == 0) s_end[0] = 0;
+    __syncthreads();
+    const int32_t T = s_end[B];
+    // warp w walks entries [e_lo, e_hi), one per lane per step
+    const int32_t e_lo = (int32_t)((int64_t)T * warp / NW);
+    const int32_t e_hi = (int32_t)((int64_t)T * (warp + 1) / NW);
+
     for (int64_t c0 = i + 1; c0 < n; c0 += win) {
         const int64_t c1 = min64(n, c0 + win);
         const int64_t words = (c1 - c0 + 1) >> 1;
+        const uint32_t wc0 = (uint32_t)c0, wlen = (uint32_t)(c1 - c0);
         for (int64_t w = tid; w < words; w += SEG_THREADS) cnt[w] = 0u;
         __syncthreads();
-        for (int b0 = warp * 32; b0 < B; b0 += NW * 32) {
-            // lane = tree b0 + lane: members of i's leaf that follow i in the
-            // run (samples > i, ascending), i.e. perm (p, end)
-            const int b = b0 + lane;
-            int32_t m = 0;
-            int64_t base = 0;
-            if (b < B) {
-                const int64_t p = (int64_t)__ldg(pos_nb + i * B + b);
-                const int64_t g = __ldg(leaf_base + b) + __ldg(codes_nb + i * B + b);
-                m = (int32_t)(__ldg(seg + g + 1) - p - 1);
-                base = p + 1;
+        // t = tree of this lane's entry: upper-bound search once, then it only
+        // moves forward
+        int t = 0;
+        {
+            const int32_t e = e_lo + lane;
+            int lo = 0, hi = B;  // largest t with s_end[t] <= e
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_end[mid] <= e) lo = mid;
+                else hi = mid;
             }
-            int32_t incl = m;
+            t = lo;
+        }
+        for (int32_t e0 = e_lo + lane; e0 < e_hi; e0 += 32 * SEG_UNROLL) {
+            uint32_t v[SEG_UNROLL];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
-            s_end[warp][lane + 1] = incl;
-            if (lane == 0) s_end[warp][0] = 0;
-            s_base[warp][lane] = base - (incl - m);  // perm index = s_base[t] + entry
-            __syncwarp();
-            // flat walk over the group's entries, one per lane: every lane busy
-            // whatever the run lengths; t = the tree of this lane's entry
-            int t = 0;
-            for (int32_t e0 = 0; e0 < total; e0 += 32 * SEG_UNROLL) {
-                uint32_t v[SEG_UNROLL];
-#pragma unroll
-                for (int u = 0; u < SEG_UNROLL; u++) {
-                    const int32_t e = e0 + u * 32 + lane;
-                    v[u] = 0xffffffffu;
-                    if (e < total) {
-                        while (s_end[warp][t + 1] <= e) t++;
-                        v[u] = __ldg(perm + s_base[warp][t] + e);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < SEG_UNROLL; u++) {
-                    if (v[u] == 0xffffffffu) continue;
-                    const int64_t j = (int64_t)(v[u] & ~RFXC_PERM_FIRST);
-                    if (j >= c0 && j < c1) {
-                        const int64_t o = j - c0;
-                        atomicAdd(cnt + (o >> 1), 1u << ((o & 1) << 4));
-                    }
+            for (int u = 0; u < SEG_UNROLL; u++) {
+                const int32_t e = e0 + u * 32;
+                v[u] = 0xffffffffu;
+                if (e < e_hi) {
+                    while (s_end[t + 1] <= e) t++;
+                    v[u] = __ldg(perm + (uint32_t)(s_base[t] + (uint32_t)e));
                 }
             }
-            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < SEG_UNROLL; u++) {
+                // column offset in the window; one unsigned compare covers both
+                // ends (and the 0xffffffff no-entry sentinel)
+                const uint32_t o = (v[u] & ~RFXC_PERM_FIRST) - wc0;
+                if (v[u] != 0xffffffffu && o < wlen)
+                    atomicAdd(cnt + (o >> 1), 1u << ((o & 1u) << 4));
+            }
         }
         __syncthreads();
+        // the row leaves once, streamed past L2 (evict-first) so the perm runs
+        // the other rows walk stay resident
         for (int64_t j = c0 + tid; j < c1; j += SEG_THREADS) {
             const int64_t o = j - c0;
             const int32_t c = (int32_t)((cnt[o >> 1] >> ((o & 1) << 4)) & 0xffffu);
             if (LAYOUT == RFXC_UPPER_I32)
-                reinterpret_cast<int32_t*>(out)[rbase + j] = c;
+                __stcs(reinterpret_cast<int32_t*>(out) + rbase + j, c);
             else if (LAYOUT == RFXC_UPPER_F64)
-                reinterpret_cast<double*>(out)[rbase + j] = (double)c / dB;
+                __stcs(reinterpret_cast<double*>(out) + rbase + j,
+                       seg_has_quot<LAYOUT>(B) ? quot[c] : (double)c / dB);
             else
-                reinterpret_cast<int32_t*>(out)[(i - row_lo) * n + j] = c;
+                __stcs(reinterpret_cast<int32_t*>(out) + (i - row_lo) * n + j, c);
         }
         __syncthreads();
     }
@@ -405,9 +460,17 @@ extern "C" int rfxc_same_leaf_pairs(const int64_t* d_seg, int64_t leaves, uint64
 template <int LAYOUT>
 static int launch_seg(const uint32_t* pos_nb, const uint32_t* perm, const int32_t* codes_nb,
                       const int64_t* seg, const int64_t* leaf_base, int64_t n, int32_t B,
-                      int64_t row_lo, int64_t row_hi, int64_t win, void* out, cudaStream_t st)
+                      int64_t row_lo, int64_t row_hi, int64_t cap, void* out, cudaStream_t st)
 {
-    const size_t smem = (size_t)((win + 1) / 2) * 4;
+    // two CTAs per SM: the counters get what the per-tree tables leave of
+    // ~100 KB (48k columns at B = 500)
+    const int64_t budget = 100 * 1024;
+    const int64_t fixed = seg_smem_bytes<LAYOUT>(0, B);
+    if (fixed > budget - 4096)
+        return fail(RFXC_EDATA, "pair_counts_leaf: B=%d too large for the shared tables", B);
+    int64_t win = std::min<int64_t>(cap, 2 * ((budget - fixed) / 4 - 2));
+    win = std::max<int64_t>(1, std::min<int64_t>(n - 1 - row_lo, win));
+    const size_t smem = (size_t)seg_smem_bytes<LAYOUT>(win, B);
     cudaError_t e = cudaFuncSetAttribute(pair_seg_kernel<LAYOUT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "pair_seg smem: %s", cudaGetErrorString(e));
@@ -425,13 +488,12 @@ extern "C" int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const uint32_t* d
     if (n < 2 || B < 1 || row_lo < 0 || row_hi > n || row_lo >= row_hi)
         return fail(RFXC_EDATA, "pair_counts_leaf: bad shape n=%lld rows=[%lld,%lld)",
                     (long long)n, (long long)row_lo, (long long)row_hi);
-    if (B > 65535) return fail(RFXC_EDATA, "pair_counts_leaf: B=%d > 65535 (16-bit counters)", B);
+    if (B > 4096) return fail(RFXC_EDATA, "pair_counts_leaf: B=%d > 4096 (shared per-tree tables)", B);
     if (row_hi - row_lo > 0x7fffffffLL) return fail(RFXC_EDATA, "pair_counts_leaf: rows");
     cudaStream_t st = as_stream(stream);
     // counters of up to 48k columns per pass: two CTAs of 512 threads per SM
-    int64_t cap = 48 * 1024;
-    if (const char* w = getenv("RFXC_PAIRS_WINDOW")) cap = std::max<int64_t>(2, atoll(w));  // tests
-    const int64_t win = std::max<int64_t>(1, std::min<int64_t>(n - 1 - row_lo, cap));
+    int64_t win = INT64_MAX;  // launch_seg sizes the window to the shared memory
+    if (const char* w = getenv("RFXC_PAIRS_WINDOW")) win = std::max<int64_t>(2, atoll(w));  // tests
     switch (layout) {
     case RFXC_UPPER_I32:
         return launch_seg<RFXC_UPPER_I32>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base, n, B, row_lo, row_hi, win, d_out, st);

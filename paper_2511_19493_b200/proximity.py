@@ -296,7 +296,7 @@ def pair_kernel(d) -> str:
     forced = os.environ.get("RFX_PAIRS_KERNEL")
     if forced in ("leaf", "tile"):
         return forced
-    if d.B > 65535 or d.n * d.Bl >= (1 << 32):
+    if d.B > 4096 or d.n * d.Bl >= (1 << 32):  # shared per-tree tables, u32 perm indices
         return "tile"
     units = d.n * (d.n - 1) // 2 * d.Bl
     return "leaf" if d.same_leaf_pairs() <= LEAF_KERNEL_MAX_SHARE * units else "tile"
