@@ -315,6 +315,10 @@ int rfxc_dequantize(const void* d_data, const double* d_scales, int64_t n,
                     int32_t r, int32_t mode, double* d_dq, void* stream);
 int rfxc_pmax(const double* d_dq, int64_t n, int32_t r, int64_t seed,
               double* d_parts, double* d_out, void* stream);
+/* The 2048 bounded draws Pcg32(seed, SEQ_PMAX).bounded(n) that rfxc_pmax
+ * pairs up (i = draw 2t, j = draw 2t+1), exactly as the sampler inside
+ * rfxc_pmax generates them (known-answer tests; proximity.py:409-417). */
+int rfxc_pmax_draws(int64_t seed, int64_t n, uint32_t* d_out, void* stream);
 
 /* ----------------------------------------------------------------- K8/K9 */
 /* Factor-space MDS power iteration (mds.py:184-268) as one persistent

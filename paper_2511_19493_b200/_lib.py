@@ -75,6 +75,7 @@ SIGNATURES = {
     "rfxc_factor_quantize": (ctypes.c_int, [P, I64, I32, P, I32, I32, P, P, P, P, P]),
     "rfxc_dequantize": (ctypes.c_int, [P, P, I64, I32, I32, P, P]),
     "rfxc_pmax": (ctypes.c_int, [P, I64, I32, I64, P, P, P]),
+    "rfxc_pmax_draws": (ctypes.c_int, [I64, I64, P, P]),
     "rfxc_mds_work_bytes": (I64, [I64, I32, I32]),
     "rfxc_mds_power": (ctypes.c_int, [P, P, P, I64, I32, F64, P, I32, I32, F64, I64, P, P, P, P,
                                       P]),

@@ -171,6 +171,53 @@ __global__ void dequant_kernel(const void* __restrict__ data, const double* __re
     }
 }
 
+// The 2048 bounded draws Pcg32(seed, SEQ_PMAX).bounded(n) of the pmax pairs
+// (proximity.py:409-417) into pairs[], by the whole (256-thread) block.
+__device__ void pmax_draws(uint64_t s0, uint64_t s1, uint32_t n, uint32_t* pairs)
+{
+    // the 2048 bounded draws of the sequential stream, generated in
+    // parallel: thread t jumps ahead to raw draw PM_PER * t, keeps the
+    // draws >= threshold (rfx_pcg32_bounded's acceptance test) and a block
+    // scan of the accept counts gives every kept draw its place in the
+    // bounded sequence; if the margin ever ran out, thread 0 redoes it
+    // sequentially (exactly the same sequence either way)
+    constexpr int PM_PER = 9;  // 256 * 9 = 2304 raw draws >= 2048 + margin
+    const uint32_t b = n;
+    const uint32_t thr = (uint32_t)((0x100000000ULL - b) % b);
+    uint64_t st[2] = {s0, s1};
+    rfx_pcg32_advance(st, (uint64_t)PM_PER * threadIdx.x);
+    uint32_t raw[PM_PER];
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < PM_PER; u++) {
+        raw[u] = rfx_pcg32_next(st);
+        cnt += raw[u] >= thr;
+    }
+    __shared__ int scan[256];
+    scan[threadIdx.x] = cnt;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {  // inclusive Hillis-Steele scan
+        const int v = threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
+        __syncthreads();
+        scan[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int pos = scan[threadIdx.x] - cnt;
+#pragma unroll
+    for (int u = 0; u < PM_PER; u++)
+        if (raw[u] >= thr) {
+            if (pos < 2048) pairs[pos] = raw[u] % b;
+            pos++;
+        }
+    const bool short_ = scan[255] < 2048;
+    __syncthreads();
+    if (short_ && threadIdx.x == 0) {
+        uint64_t s[2] = {s0, s1};
+        for (int t = 0; t < 2048; t++) pairs[t] = rfx_pcg32_bounded(s, b);
+    }
+    __syncthreads();
+}
+
 // pmax: block q < nparts -> max of diag over its rows; last block -> the
 // 1024 sampled pairs (Pcg32(seed, SEQ_PMAX), i == j skipped, no redraw).
 __global__ void __launch_bounds__(256)
@@ -178,7 +225,7 @@ pmax_kernel(const double* __restrict__ dq, int64_t n, int r, int64_t rows_per_pa
             uint64_t s0, uint64_t s1, double* __restrict__ parts)
 {
     __shared__ double red[32];
-    __shared__ int pairs[2048];
+    __shared__ uint32_t pairs[2048];
     double m = -INFINITY;
     if ((int)blockIdx.x < nparts) {
         const int64_t r0 = blockIdx.x * rows_per_part, r1 = min(n, r0 + rows_per_part);
@@ -188,47 +235,7 @@ pmax_kernel(const double* __restrict__ dq, int64_t n, int r, int64_t rows_per_pa
             m = fmax(m, s);
         }
     } else {
-        // the 2048 bounded draws of the sequential stream, generated in
-        // parallel: thread t jumps ahead to raw draw PM_PER * t, keeps the
-        // draws >= threshold (rfx_pcg32_bounded's acceptance test) and a block
-        // scan of the accept counts gives every kept draw its place in the
-        // bounded sequence; if the margin ever ran out, thread 0 redoes it
-        // sequentially (exactly the same sequence either way)
-        constexpr int PM_PER = 9;  // 256 * 9 = 2304 raw draws >= 2048 + margin
-        const uint32_t b = (uint32_t)n;
-        const uint32_t thr = (uint32_t)((0x100000000ULL - b) % b);
-        uint64_t st[2] = {s0, s1};
-        rfx_pcg32_advance(st, (uint64_t)PM_PER * threadIdx.x);
-        uint32_t raw[PM_PER];
-        int cnt = 0;
-#pragma unroll
-        for (int u = 0; u < PM_PER; u++) {
-            raw[u] = rfx_pcg32_next(st);
-            cnt += raw[u] >= thr;
-        }
-        __shared__ int scan[256];
-        scan[threadIdx.x] = cnt;
-        __syncthreads();
-        for (int o = 1; o < 256; o <<= 1) {  // inclusive Hillis-Steele scan
-            const int v = threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
-            __syncthreads();
-            scan[threadIdx.x] += v;
-            __syncthreads();
-        }
-        int pos = scan[threadIdx.x] - cnt;
-#pragma unroll
-        for (int u = 0; u < PM_PER; u++)
-            if (raw[u] >= thr) {
-                if (pos < 2048) pairs[pos] = (int)(raw[u] % b);
-                pos++;
-            }
-        const bool short_ = scan[255] < 2048;
-        __syncthreads();
-        if (short_ && threadIdx.x == 0) {
-            uint64_t s[2] = {s0, s1};
-            for (int t = 0; t < 2048; t++) pairs[t] = (int)rfx_pcg32_bounded(s, b);
-        }
-        __syncthreads();
+        pmax_draws(s0, s1, (uint32_t)n, pairs);
         for (int t = threadIdx.x; t < 1024; t += blockDim.x) {
             const int64_t i = pairs[2 * t], j = pairs[2 * t + 1];
             if (i == j) continue;
@@ -239,6 +246,15 @@ pmax_kernel(const double* __restrict__ dq, int64_t n, int r, int64_t rows_per_pa
     }
     m = block_max(m, red);
     if (threadIdx.x == 0) parts[blockIdx.x] = m;
+}
+
+__global__ void __launch_bounds__(256) pmax_draws_kernel(uint64_t s0, uint64_t s1, uint32_t n,
+                                                         uint32_t* __restrict__ out)
+{
+    __shared__ uint32_t pairs[2048];
+    pmax_draws(s0, s1, n, pairs);
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2048; t += blockDim.x) out[t] = pairs[t];
 }
 
 __global__ void max_final_kernel(const double* __restrict__ parts, int np, double* out)
@@ -319,6 +335,15 @@ extern "C" int rfxc_dequantize(const void* d_data, const double* d_scales, int64
     const int grid = (int)std::min<int64_t>(ceil_div(n * r, 256), (int64_t)sm_count() * 16);
     dequant_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_data, d_scales, n, r, mode, d_dq);
     return check_launch("dequantize");
+}
+
+extern "C" int rfxc_pmax_draws(int64_t seed, int64_t n, uint32_t* d_out, void* stream)
+{
+    if (n < 1 || n > UINT32_MAX) return fail(RFXC_EDATA, "pmax_draws: bad n");
+    uint64_t s[2];
+    rfx_pcg32_make(seed, RFX_SEQ_PMAX, s);
+    pmax_draws_kernel<<<1, 256, 0, as_stream(stream)>>>(s[0], s[1], (uint32_t)n, d_out);
+    return check_launch("pmax_draws");
 }
 
 extern "C" int rfxc_pmax(const double* d_dq, int64_t n, int32_t r, int64_t seed, double* d_parts,

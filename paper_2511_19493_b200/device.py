@@ -184,7 +184,7 @@ class DeviceValues:
     def f64(self):
         torch = _torch()
         if self._f64 is None:
-            self._f64 = torch.from_numpy(np.ascontiguousarray(self._host.T)).to(self.dev)
+            self._f64 = torch.from_numpy(np.require(self._host.T, requirements=["C", "W"])).to(self.dev)
         return self._f64
 
 

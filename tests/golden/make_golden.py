@@ -57,6 +57,16 @@ def pcg_kats():
     return out
 
 
+def pmax_draw_kats():
+    """The 2048 bounded draws of the pmax pair sampler, Pcg32(seed, 4)
+    (proximity.py:409-417), for a few (seed, n)."""
+    out = []
+    for seed, n in [(0, 178), (5, 2000), (0, 100_000), (-3, 2**31 + 11), (7, 3)]:
+        g = Pcg32(seed, 4)
+        out.append(dict(seed=seed, n=n, draws=[int(g.bounded(n)) for _ in range(2048)]))
+    return out
+
+
 def lowrank_record(mem, rank, mode, seed):
     lr = rprox.lowrank_proximity(mem, rank=rank, mode=mode, seed=seed)
     rec = dict(rank=lr.rank, degraded=lr.rank_degraded, pmax=lr.pmax,
@@ -145,6 +155,8 @@ def small():
                         points=pts, codes=hb)
     with open(os.path.join(HERE, "pcg32.json"), "w") as fh:
         json.dump(pcg_kats(), fh, indent=1)
+    with open(os.path.join(HERE, "pcg32_pmax.json"), "w") as fh:
+        json.dump(pmax_draw_kats(), fh)
     with open(os.path.join(HERE, "fixtures.json"), "w") as fh:
         json.dump(fx, fh, indent=1, sort_keys=True)
 
@@ -189,5 +201,10 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", action="store_true")
     ap.add_argument("--only", nargs="*", help="scale configs to (re)generate, e.g. 100k")
+    ap.add_argument("--pmax-kats", action="store_true", help="only tests/golden/pcg32_pmax.json")
     a = ap.parse_args()
-    scale(a.only) if a.scale else small()
+    if a.pmax_kats:
+        with open(os.path.join(HERE, "pcg32_pmax.json"), "w") as fh:
+            json.dump(pmax_draw_kats(), fh)
+    else:
+        scale(a.only) if a.scale else small()

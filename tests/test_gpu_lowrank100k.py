@@ -1,6 +1,13 @@
 """BASELINE configs[3] at full size: synthetic 100k x 100, 500 trees (the
-bench workload).  The oracle pipeline takes minutes here, so the sketch and
-the factor are checked through size-independent properties:
+bench workload).
+
+Pinned to the REFERENCE run at this size (tests/golden/scale.json["100k"] and
+lowrank_100k.npz, from make_golden.py --scale --only 100k): the regrown
+forest's RFX1 SHA-256, the (n, B) leaf codes' SHA-256, and the reference's
+rank-32 INT8 factor, pmax and 3-D MDS embedding at the stated tolerances
+(relative Frobenius 1e-4, pmax 1e-4, eigenvalues rtol 1e-5, Procrustes 1e-5).
+
+Size-independent properties of the sketch and the factor on top:
 
 * P 1 (a sketch pass of the all-ones column) equals (1/B) sum_b s_{b,l_b(i)}
   from the leaf sizes — exact integers in f32, rtol 1e-12;
@@ -20,16 +27,21 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs C
 
 
 @pytest.fixture(scope="module")
-def mem100k(built):
+def inputs100k(built):
     import os
 
-    from paper_2511_19493_b200 import proximity as P
-    from paper_2511_19493_b200.dataset import from_arrays, make_synthetic
     from oracle.trainer import train
+    from paper_2511_19493_b200.dataset import from_arrays, make_synthetic
     from paper_2511_19493_b200.forest import TrainConfig
     X, y = make_synthetic(100_000, 100, seed=0)
     ds = from_arrays(X, y)
-    forest = train(ds, TrainConfig(ntree=500, iseed=1), nthreads=os.cpu_count() or 1)
+    return ds, train(ds, TrainConfig(ntree=500, iseed=1), nthreads=os.cpu_count() or 1)
+
+
+@pytest.fixture(scope="module")
+def mem100k(inputs100k):
+    from paper_2511_19493_b200 import proximity as P
+    ds, forest = inputs100k
     return P.leaf_membership(forest, ds)
 
 
@@ -86,3 +98,34 @@ def test_factor_captures_the_top_of_P(mem100k):
     uQQu = float(np.sum((Q.T @ u) ** 2))
     assert abs(uPu - uQQu) <= 1e-3 * uPu, (uPu, uQQu)
     assert 0.0 < lr.pmax <= 1.0 + 1e-6
+
+
+def test_forest_and_codes_are_the_references(inputs100k, mem100k):
+    import hashlib
+    import json
+    import os
+
+    from conftest import GOLDEN
+    from paper_2511_19493_b200.forest import forest_to_bytes
+    rec = json.load(open(os.path.join(GOLDEN, "scale.json")))["100k"]
+    ds, forest = inputs100k
+    assert hashlib.sha256(forest_to_bytes(forest)).hexdigest() == rec["rfx1_sha"]
+    assert hashlib.sha256(mem100k.codes.tobytes()).hexdigest() == rec["codes_sha"]
+    assert int(mem100k.leaf_counts.sum()) == rec["total_leaves"]
+
+
+def test_factor_and_mds_vs_reference(mem100k):
+    from conftest import golden
+    from paper_2511_19493_b200 import mds as M
+    from paper_2511_19493_b200 import proximity as P
+    from test_gpu_lowrank import frob_rel
+    from test_gpu_mds import procrustes_rel
+    g = golden("lowrank_100k.npz")
+    lr = P.lowrank_proximity(mem100k, rank=32, mode="i8", seed=0)
+    ref = g["data"].astype(np.float64) * g["scales"][None, :]
+    assert frob_rel(lr.dequantized(), ref) <= 1e-4
+    assert abs(lr.pmax - float(g["pmax"])) / float(g["pmax"]) <= 1e-4
+    emb = M.mds_lowrank(lr, M.PowerIterConfig(seed=0))
+    np.testing.assert_allclose(emb.eigenvalues, g["mds_eig"], rtol=1e-5)
+    assert procrustes_rel(emb.coordinates, g["mds_coords"]) <= 1e-5
+    assert np.all(np.abs(np.asarray(emb.iterations) - g["mds_iter"]) <= 2)
