@@ -72,8 +72,11 @@ __global__ void outlier_final_kernel(const double* __restrict__ rowsum,
 }
 
 // ------------------------------------------------------------- low rank
-constexpr int OL_I = 128;  // rows per CTA (16 warps x 8)
-constexpr int OL_J = 64;   // streamed column block
+// Rows per CTA = 8 * WARPS, streamed column block OL_J: <16, 64> keeps 128
+// rows of Q_I in shared memory; ranks whose (128 + 2 * 64) rows exceed it
+// run <4, 32> (32 rows, 32-row column blocks).  Every lane sums the columns
+// j = 2 fr + h (mod 8) in ascending order in both, so the scores are the same
+// bits whichever variant runs.
 
 __host__ __device__ inline int ol_ld(int rp) { return rp + ((4 - rp % 16) + 16) % 16; }
 
@@ -84,10 +87,12 @@ __device__ __forceinline__ void ol_cp8(void* smem, const void* gmem, bool ok)
                  : "memory");
 }
 
-__global__ void __launch_bounds__(512, 1)
+template <int WARPS, int OL_J>
+__global__ void __launch_bounds__(WARPS * 32, 1)
 outlier_lowrank_kernel(const double* __restrict__ Q, int64_t n, int r, double floor_,
                        double* __restrict__ scores)
 {
+    constexpr int OL_I = 8 * WARPS;
     extern __shared__ __align__(16) double osm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int fr = lane & 3, fc = lane >> 2;
@@ -188,15 +193,22 @@ extern "C" int rfxc_outlier_lowrank(const double* d_dq, int64_t n, int32_t r, do
     if (r < 1 || r > 256) return fail(RFXC_EDATA, "outlier_lowrank: rank %d outside [1, 256]", r);
     if (!(floor_ > 0.0)) return fail(RFXC_EDATA, "clamp_floor must be positive");
     const int rp = (r + 3) / 4 * 4, lq = ol_ld(rp);
-    const size_t smem = (size_t)(OL_I + 2 * OL_J) * lq * 8;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(outlier_lowrank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
+        cudaFuncSetAttribute(outlier_lowrank_kernel<16, 64>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(outlier_lowrank_kernel<4, 32>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    if (smem > 227 * 1024) return fail(RFXC_EDATA, "outlier_lowrank: rank %d too large", r);
-    outlier_lowrank_kernel<<<(unsigned)ceil_div(n, OL_I), 512, smem, as_stream(stream)>>>(
-        d_dq, n, r, floor_, d_scores);
+    const size_t big = (size_t)(128 + 2 * 64) * lq * 8, small = (size_t)(32 + 2 * 32) * lq * 8;
+    if (big <= 227 * 1024)
+        outlier_lowrank_kernel<16, 64><<<(unsigned)ceil_div(n, 128), 512, big,
+                                         as_stream(stream)>>>(d_dq, n, r, floor_, d_scores);
+    else if (small <= 227 * 1024)
+        outlier_lowrank_kernel<4, 32><<<(unsigned)ceil_div(n, 32), 128, small,
+                                       as_stream(stream)>>>(d_dq, n, r, floor_, d_scores);
+    else
+        return fail(RFXC_EDATA, "outlier_lowrank: rank %d too large", r);
     return check_launch("outlier_lowrank");
 }

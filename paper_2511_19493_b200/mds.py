@@ -93,6 +93,9 @@ def mds_full(prox, k: int = 3, oracle_bound: int = DEFAULT_ORACLE_BOUND) -> MdsE
                         np.ones(kp, dtype=bool))
 
 
+MAX_RANK = 192  # rfxc_mds_power / rfxc_gram_matvec (csrc/mds.cu MAXRT)
+
+
 def _work(n: int, r: int, k: int, dev):
     import torch
     nbytes = int(_lib.load().rfxc_mds_work_bytes(n, r, k))
@@ -105,6 +108,8 @@ def gram_matvec(lowrank: LowRankQuantized, v: np.ndarray, _cache: dict | None = 
     v = np.asarray(v, dtype=np.float64)
     if v.shape != (lowrank.n,):
         raise DataError(f"vector length {v.shape} does not match n={lowrank.n}")
+    if int(lowrank.rank) > MAX_RANK:
+        raise DataError(f"gram_matvec: rank {lowrank.rank} above this build's limit {MAX_RANK}")
     dq = lowrank.dequantized_device()
     n, r = dq.shape
     dv = torch.from_numpy(np.ascontiguousarray(v)).to(dq.device)
@@ -119,6 +124,9 @@ def mds_lowrank_device(lowrank: LowRankQuantized, config: PowerIterConfig | None
     (coords (n, k), info (k, 4), k_used (1,))."""
     import torch
     cfg = config or PowerIterConfig()
+    r = int(lowrank.rank)
+    if r > MAX_RANK:  # before any upload or launch (INTEGRATION.md "Limits")
+        raise DataError(f"mds_lowrank: rank {r} above this build's limit {MAX_RANK}")
     dq = lowrank.dq if hasattr(lowrank, "dq") else lowrank.dequantized_device()
     n, r = dq.shape
     dev = dq.device

@@ -104,11 +104,7 @@ class LeafMembership:
     def total_leaves(self) -> int:
         """Leaves over the whole forest (all-reduced over the ranks when this
         membership is a tree shard)."""
-        local = int(self.leaf_counts.sum())
-        if self._dev is None or not self._dev.is_shard:
-            return local
-        from .distributed import all_reduce_int
-        return all_reduce_int(local)
+        return _total_leaves(self)
 
     @property
     def tree_range(self):
@@ -245,12 +241,26 @@ class FullTriangle:
 
 
 def _device_budget(nbytes: int, what: str, n: int, B: int):
+    """Refuse (BudgetError + planner dict) a device allocation that cannot fit:
+    free device memory plus the blocks torch has cached but not handed out."""
     import torch
     free, _total = torch.cuda.mem_get_info()
+    free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
     if nbytes > free:
         raise BudgetError(f"{what} for n={n} needs {nbytes} bytes of device memory, "
                           f"{free} free; shard rows across GPUs or use the lowrank backend",
                           memory_plan(n, tree_count=B))
+
+
+def _device_empty(numel: int, dtype, dev, what: str, n: int, B: int):
+    """torch.empty on the device, an out-of-memory error mapped to BudgetError."""
+    import torch
+    try:
+        return torch.empty(numel, dtype=dtype, device=dev)
+    except torch.OutOfMemoryError as e:
+        raise BudgetError(f"{what} for n={n}: device allocation of {numel} elements failed "
+                          f"({e}); shard rows across GPUs or use the lowrank backend",
+                          memory_plan(n, tree_count=B)) from e
 
 
 def pair_counts_device(membership: LeafMembership, layout: int, row_lo: int = 0,
@@ -268,7 +278,7 @@ def pair_counts_device(membership: LeafMembership, layout: int, row_lo: int = 0,
         numel = _row_start(n, row_hi) - _row_start(n, row_lo)
         dt = torch.float64 if layout == _lib.UPPER_F64 else torch.int32
     _device_budget(numel * (8 if dt == torch.float64 else 4), "pair counts", n, B)
-    out = torch.empty(max(numel, 1), dtype=dt, device=d.codes_nb.device)
+    out = _device_empty(max(numel, 1), dt, d.codes_nb.device, "pair counts", n, B)
     if n >= 2 and row_hi > row_lo:
         if pair_kernel(d) == "leaf":
             pos, (perm, seg) = d.positions(), d.buckets()
@@ -746,6 +756,25 @@ def _ritz_factor_map(T, k: int, r: int):
     return Wr
 
 
+# Limit of the device kernels (INTEGRATION.md "Limits"): the factor /
+# quantisation and outlier kernels take r <= 256 columns, the MDS kernel
+# r <= 192; lowrank_proximity refuses ranks above 192 up front so every factor
+# it returns can go on through mds_lowrank and outlier_scores.
+MAX_RANK = 192
+
+
+def _total_leaves(membership: LeafMembership, group=None) -> int:
+    """Leaves over the whole forest: a tree shard sums its own over ``group``
+    (the ranks holding the other shards), exactly the group the sketch
+    all-reduces over."""
+    d = membership._dev
+    local = int(membership.leaf_counts.sum())
+    if d is None or not d.is_shard:
+        return local
+    from .distributed import all_reduce_int
+    return all_reduce_int(local, group)
+
+
 def lowrank_device(membership: LeafMembership, rank: int, mode: str = "i8", seed: int = 0,
                    group=None) -> "DeviceLowRank":
     """The device pipeline behind lowrank_proximity (results stay in HBM)."""
@@ -755,7 +784,10 @@ def lowrank_device(membership: LeafMembership, rank: int, mode: str = "i8", seed
     n = membership.n
     if rank < 1:
         raise DataError(f"rank must be >= 1, got {rank}")
-    bound = min(n, membership.total_leaves)
+    bound = min(n, _total_leaves(membership, group))
+    if min(rank, bound) > MAX_RANK:
+        raise DataError(f"rank {min(rank, bound)} above this build's limit {MAX_RANK} "
+                        f"(the MDS kernel's; INTEGRATION.md 'Limits')")
     degraded = rank > bound
     if degraded:
         logger.warning("requested rank %d exceeds membership rank bound %d; "

@@ -61,7 +61,7 @@ def test_wine_matches_reference_scores(built):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not cuda_ok(), reason="needs CUDA")
-@pytest.mark.parametrize("n,r", [(2, 1), (130, 3), (2000, 32), (3001, 40)])
+@pytest.mark.parametrize("n,r", [(2, 1), (130, 3), (2000, 32), (3001, 40), (500, 110), (701, 150), (333, 256)])
 def test_lowrank_kernel_vs_oracle(built, n, r):
     from paper_2511_19493_b200 import proximity as P
     from paper_2511_19493_b200.quantize import QuantFactor
