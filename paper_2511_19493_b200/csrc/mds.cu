@@ -46,6 +46,7 @@ constexpr int BS = 24;         // reduction-B slots
 constexpr int MAXRT = 24;      // r <= 192
 constexpr int SMS_MAXRP = 96;  // S kept in shared memory up to RP = 96
 constexpr int SMEM_BUDGET = 222 * 1024;  // + ~3 KB of static shared memory
+constexpr int MDS_I8F_THREADS = 256;     // int8-resident fast path (r <= 32)
 
 enum { QS_F64 = 0, QS_I8 = 1, QS_GLOBAL = 2 };
 
@@ -55,6 +56,7 @@ struct MdsArgs {
     const double* scales;   // (r) per-column scales (QS_I8)
     int64_t n;
     int r;
+    int r8;                 // row stride of the int8 slice (RP: columns >= r are zero)
     double pmax;
     const double* pmax_dev;  // when set, pmax is read from device memory (rfxc_pmax's output)
     int k;
@@ -111,6 +113,7 @@ struct Sm {
     double* bc;         // BS broadcast slots
     double* kc;         // 2 constants
     int* tab;           // NT x 2 tile coordinates
+    double* buf;        // QS_I8 (RT <= 4): warps x NV x 32 cross-warp partials
 };
 
 __host__ __device__ __forceinline__ int rp_of(int r) { return 8 * ((r + 7) / 8); }
@@ -125,7 +128,7 @@ __device__ __forceinline__ double qp(const MdsArgs& A, const Sm& s, int64_t r0, 
 {
     if (c < A.r) {
         if (QS == QS_F64) return s.q64[i * s.ldq + c];
-        if (QS == QS_I8) return (double)s.q8[i * A.r + c] * s.sc[c];
+        if (QS == QS_I8) return (double)s.q8[i * A.r8 + c] * s.sc[c];
         return __ldg(A.dq + (r0 + i) * A.r + c);
     }
     return c == A.r ? 1.0 : 0.0;
@@ -136,7 +139,7 @@ template <int QS>
 __device__ __forceinline__ double qraw(const MdsArgs& A, const Sm& s, int64_t r0, int64_t i, int c)
 {
     if (QS == QS_F64) return s.q64[i * s.ldq + c];
-    if (QS == QS_I8) return (double)s.q8[i * A.r + c] * s.sc[c];
+    if (QS == QS_I8) return (double)s.q8[i * A.r8 + c] * s.sc[c];
     return __ldg(A.dq + (r0 + i) * A.r + c);
 }
 
@@ -315,6 +318,95 @@ __device__ void spass4(const MdsArgs& A, const Sm& s, int64_t rows, const double
     }
 }
 
+// S'(x) partial of this CTA for the int8-resident slice (codes c, per-column
+// scales s; q = c * s), r <= 8 * RT, RT <= 4, every warp of the CTA on the
+// FP64 tensor cores: warp w takes a contiguous share of the 4-row k-steps
+// and accumulates the whole upper triangle of S_c = sum_i x_i c_i c_i^T
+// (integer codes are exact in f64: A = x * c, B = c), t_c = sum x c and
+// sum x; the warps' partials meet in shared memory `buf` (warps x NV x 32
+// doubles) and are added in warp order; the CTA partial is written in the
+// q-space (S_ab = s_a s_b S_c,ab, t_a = s_a t_c,a) the reductions use.
+template <int RT, typename Extra>
+__device__ void spass_i8(const MdsArgs& A, const Sm& s, int64_t rows, const double* x, double* buf,
+                         Extra&& extra)
+{
+    constexpr int NP = RT * (RT + 1) / 2;
+    constexpr int NV = 2 * NP + RT + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (int)(blockDim.x >> 5);
+    const int fr = lane & 3, fc = lane >> 2;
+    const int r = A.r;
+    double* out = A.sparts + (int64_t)blockIdx.x * A.PE;
+    double v[NV];
+#pragma unroll
+    for (int j = 0; j < NV; j++) v[j] = 0.0;
+    {
+        const int nks = (int)(pad16(rows) >> 2);
+        const int k0 = warp * nks / nw, k1 = (warp + 1) * nks / nw;
+        // lane's columns 8t + fc of the zero-padded slice (codes beyond r are 0)
+        const int8_t* pq = s.q8 + fc;
+        const int ldc = A.r8;
+#pragma unroll 2
+        for (int ks = k0; ks < k1; ks++) {
+            const int i = 4 * ks + fr;
+            const double xq = x[i];
+            double b[RT], a[RT];
+#pragma unroll
+            for (int t = 0; t < RT; t++) {
+                b[t] = (double)pq[i * ldc + 8 * t];
+                a[t] = xq * b[t];
+                v[2 * NP + t] += a[t];
+            }
+            v[2 * NP + RT] += xq;
+            int pi = 0;
+#pragma unroll
+            for (int ta = 0; ta < RT; ta++)
+#pragma unroll
+                for (int tb = ta; tb < RT; tb++, pi++) dmma884(v[2 * pi], v[2 * pi + 1], a[ta], b[tb]);
+        }
+#pragma unroll
+        for (int j = 2 * NP; j < NV; j++) {
+            v[j] += __shfl_xor_sync(0xffffffffu, v[j], 1);
+            v[j] += __shfl_xor_sync(0xffffffffu, v[j], 2);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; j++) buf[(warp * NV + j) * 32 + lane] = v[j];
+    extra((int)threadIdx.x, (int)blockDim.x);  // the caller's row sums meanwhile
+    __syncthreads();
+    // value (j, lane) of the CTA partial: the warps' values in warp order
+    const int RTq = (r + 7) / 8, tbr = r >> 3;
+    for (int e = threadIdx.x; e < NV * 32; e += (int)blockDim.x) {
+        const int j = e >> 5, ln = e & 31, efr = ln & 3, efc = ln >> 2;
+        double acc = 0.0;
+        for (int w = 0; w < nw; w++) acc += buf[(w * NV + j) * 32 + ln];
+        if (j < 2 * NP) {
+            // tile pi = j / 2, fragment element (efc, 2 efr + j % 2)
+            int pi = j >> 1, ta = 0;
+            while (pi >= RT - ta) { pi -= RT - ta; ta++; }
+            const int tb = ta + pi;
+            if (tb >= RTq) continue;
+            const int a = 8 * ta + efc, bcol = 8 * tb + 2 * efr + (j & 1);
+            // (a, r) and (r, r) are the t / sum slots written below; every
+            // other entry beyond the factor is zero padding
+            if ((bcol == r && a <= r)) continue;
+            const int t = ta * A.TP - ta * (ta - 1) / 2 + (tb - ta);
+            out[t * 64 + efc * 8 + 2 * efr + (j & 1)] =
+                (a < r && bcol < r) ? (s.sc[a] * s.sc[bcol]) * acc : 0.0;
+        } else if (j < 2 * NP + RT) {
+            if (efr != 0) continue;  // the four row phases were already added
+            const int a = 8 * (j - 2 * NP) + efc;
+            if (a < r) {
+                const int ta = a >> 3;
+                out[(ta * A.TP - ta * (ta - 1) / 2 + (tbr - ta)) * 64 + (a & 7) * 8 + (r & 7)] =
+                    s.sc[a] * acc;
+            }
+        } else if (ln == 0) {
+            out[(tbr * A.TP - tbr * (tbr - 1) / 2) * 64 + (r & 7) * 8 + (r & 7)] = acc;
+        }
+    }
+}
+
 // fixed-order block reduction of m <= 16 per-thread values into out[0..m)
 // (warp trees, then the warp partials in warp order); red >= 16 * warps
 __device__ void block_sums(double* v, int m, double* red, double* out)
@@ -455,6 +547,30 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int fr = lane & 3, fc = lane >> 2;
     const int KS = (r + 3) / 4;
+    // int8 fast path: the lane's fragments of S~ = D S D (D = diag(scales), so
+    // the A operands are the exact integer codes) and of t~ = D t stay in
+    // registers for the whole row loop
+    constexpr bool I8F = QS == QS_I8 && SMS && RT <= 4;
+    constexpr int NPF = RT * (RT + 1) / 2;
+    double sf[I8F ? 2 * NPF : 1], tf[I8F ? 2 * RT : 1];
+    if constexpr (I8F) {
+        int pi = 0;
+#pragma unroll
+        for (int ta = 0; ta < RT; ta++)
+#pragma unroll
+            for (int tb = ta; tb < RT; tb++, pi++)
+#pragma unroll
+                for (int ks = 0; ks < 2; ks++) {
+                    const int kr = 8 * ta + 4 * ks + fr, col = 8 * tb + fc;
+                    const double sk = kr < r ? s.sc[kr] : 0.0, sc2 = col < r ? s.sc[col] : 0.0;
+                    sf[2 * pi + ks] = (sk * s.S[kr * (RP + 4) + col]) * sc2;
+                }
+#pragma unroll
+        for (int j = 0; j < 2 * RT; j++) {
+            const int col = 4 * j + fr;
+            tf[j] = col < r ? s.sc[col] * s.t[col] : 0.0;
+        }
+    }
     for (int64_t row0 = 8 * (int64_t)warp; row0 < rows; row0 += 8 * (int)(blockDim.x >> 5)) {
         const int64_t ia = row0 + fc;  // fragment / output row of this lane
         const bool va = ia < rows;
@@ -462,7 +578,47 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
 #pragma unroll
         for (int tn = 0; tn < RT; tn++) acc[tn][0] = acc[tn][1] = 0.0;
         double ppu = 0.0, pu = 0.0;
-        if constexpr (QS == QS_F64 && SMS) {
+        if constexpr (I8F) {
+            // the lane's 4 RT codes of the row: A-fragment columns 4 j + fr and the
+            // epilogue columns 8 tb + 2 fr + h (zero-padded slice: rows to 16,
+            // columns to RP), converted exactly to f64
+            const int8_t* row = s.q8 + ia * A.r8;
+            int wv[2 * RT];
+#pragma unroll
+            for (int j = 0; j < 2 * RT; j++) wv[j] = reinterpret_cast<const int*>(row)[j];
+            double af[2 * RT], ep[2 * RT];
+#pragma unroll
+            for (int j = 0; j < 2 * RT; j++) {
+                af[j] = (double)(int8_t)(wv[j] >> (8 * fr));
+                // column 8 tb + 2 fr + h: word 2 tb + fr / 2, byte (2 fr + h) & 3
+                const int w = fr >= 2 ? wv[(j & ~1) + 1] : wv[j & ~1];
+                ep[j] = (double)(int8_t)(w >> (8 * ((2 * fr + (j & 1)) & 3)));
+            }
+            double z[NPF][2];
+#pragma unroll
+            for (int pi = 0; pi < NPF; pi++) z[pi][0] = z[pi][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 2; ks++) {
+                int pi = 0;
+#pragma unroll
+                for (int ta = 0; ta < RT; ta++)
+#pragma unroll
+                    for (int tb = ta; tb < RT; tb++, pi++)
+                        dmma884(z[pi][0], z[pi][1], af[2 * ta + ks], sf[2 * pi + ks]);
+            }
+            {
+                int pi = 0;
+#pragma unroll
+                for (int ta = 0; ta < RT; ta++)
+#pragma unroll
+                    for (int tb = ta; tb < RT; tb++, pi++) {
+                        const double wgt = ta == tb ? 1.0 : 2.0;
+                        ppu += wgt * (z[pi][0] * ep[2 * tb] + z[pi][1] * ep[2 * tb + 1]);
+                    }
+            }
+#pragma unroll
+            for (int j = 0; j < 2 * RT; j++) pu += af[j] * tf[j];
+        } else if constexpr (QS == QS_F64 && SMS) {
             // q^T S q over the upper-triangle tile pairs of the symmetric S:
             // Z = Q_(ta) S_(ta,tb) (2 k-steps), then ppu += w Z . Q_(tb)
             const double* pq = s.q64 + ia * s.ldq;
@@ -586,7 +742,9 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     const int64_t r0 = min64(n, blockIdx.x * A.rpb);
     const int64_t rows = min64(n, r0 + A.rpb) - r0;
 
-    // shared memory: [S RPxRP if SMS] [t RP] [us rpb] [scales r] [codes rows x r]
+    // shared memory: [S RPxRP if SMS] [t RP] [us rpb] [scales r] [codes pad16(rpb) x RP]
+    // [I8F: cross-warp partials warps x NV x 32]
+    constexpr bool I8F = QS == QS_I8 && SMS && RT <= 4;
     Sm s;
     s.S = reinterpret_cast<double*>(msm);
     s.t = s.S + (SMS ? RP * (RP + 4) : 0);
@@ -601,6 +759,7 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     s.bc = bc;
     s.kc = kc;
     s.tab = tab;
+    s.buf = scs + r + (pad16(A.rpb) * RP + 7) / 8;
     if (threadIdx.x == 0) {
         int t = 0;
         for (int a = 0; a < A.TP; a++)
@@ -613,7 +772,12 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     if (QS == QS_I8) {
         int8_t* q8 = reinterpret_cast<int8_t*>(scs + r);
         for (int e = threadIdx.x; e < r; e += (int)blockDim.x) scs[e] = A.scales[e];
-        for (int64_t e = threadIdx.x; e < rows * r; e += (int)blockDim.x) q8[e] = A.codes[r0 * r + e];
+        // zero-padded to pad16(rpb) rows x RP columns (A.r8 = RP)
+        for (int64_t e = threadIdx.x; e < pad16(A.rpb) * RP; e += (int)blockDim.x) {
+            const int64_t i = e / RP;
+            const int c = (int)(e % RP);
+            q8[e] = (i < rows && c < r) ? A.codes[(r0 + i) * r + c] : (int8_t)0;
+        }
     } else if (QS == QS_F64) {  // zero-padded to pad16(rpb) rows x ldq columns
         double* q64 = scs + r;
         const int64_t tot = pad16(A.rpb) * s.ldq;
@@ -632,7 +796,9 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     // S' reduction of s.us; `extra(t0, stride)` (row sums over rows t0, t0 +
     // stride, ...) runs on the warps the reduction leaves idle
     auto sreduce = [&](auto&& extra) {
-        if constexpr (SP4) {
+        if constexpr (I8F) {
+            spass_i8<RT>(A, s, rows, s.us, s.buf, extra);
+        } else if constexpr (SP4) {
             spass4<RT>(A, s, rows, s.us, s.S, [&]() {
                 extra((int)threadIdx.x - 32 * SP_W, (int)blockDim.x - 32 * SP_W);
             });
@@ -949,14 +1115,24 @@ static size_t plan_smem(MdsArgs& A)
     const size_t fixed =
         ((sms ? (size_t)RP * (RP + 4) : 0) + RP + (size_t)pad16(A.rpb) + r) * 8;
     const size_t f64 = (size_t)pad16(A.rpb) * ldq_of(RP) * 8;
-    const size_t i8 = (size_t)A.rpb * r;
+    const size_t i8 = ((size_t)pad16(A.rpb) * RP + 7) / 8 * 8;
+    A.r8 = RP;
+    // int8-resident slice with the all-warp DMMA reduction and the
+    // register-resident row pass (r <= 32): preferred whenever the codes exist
+    const bool fast = A.codes && sms && RP <= 32 && !getenv("RFXC_MDS_F64");
+    const int RTf = RP / 8, NV = RTf * (RTf + 1) + RTf + 1;
+    const size_t fbuf = (size_t)(MDS_I8F_THREADS / 32) * NV * 32 * 8;
+    if (fast && fixed + i8 + fbuf <= SMEM_BUDGET) {
+        A.qs = QS_I8;
+        return fixed + i8 + fbuf;
+    }
     if (fixed + f64 <= SMEM_BUDGET) {
         A.qs = QS_F64;
         return fixed + f64;
     }
-    if (A.codes && fixed + i8 <= SMEM_BUDGET) {
+    if (A.codes && fixed + i8 + (RP <= 32 ? fbuf : 0) <= SMEM_BUDGET) {  // (r <= 32: fast path)
         A.qs = QS_I8;
-        return fixed + i8;
+        return fixed + i8 + (RP <= 32 ? fbuf : 0);
     }
     A.qs = QS_GLOBAL;
     return fixed;
@@ -965,8 +1141,9 @@ static size_t plan_smem(MdsArgs& A)
 template <int QS, int RT>
 static int launch_q(MdsArgs& A, size_t smem, cudaStream_t st)
 {
-    // 16 warps while the row-pass accumulators fit 128 registers, else 8
-    constexpr int NTH = RT <= 8 ? 512 : 256;
+    // 16 warps while the row-pass accumulators fit 128 registers, else 8; the
+    // int8 fast path keeps S fragments in registers: 8 warps
+    constexpr int NTH = (QS == QS_I8 && RT <= 4) ? MDS_I8F_THREADS : (RT <= 8 ? 512 : 256);
     auto kern = mds_kernel<QS, RT, NTH>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 1));
