@@ -19,6 +19,8 @@
 // f32-exact (checked by rfxc_values_to_f32; otherwise the f64 layout runs).
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace rfxc {
 
 // ---------------------------------------------------------------- K0 pack
@@ -125,7 +127,13 @@ constexpr int TRAV_T = 128;             // samples per CTA (one X row each in sh
 constexpr int TRAV_G = RFXC_TRAV_G;     // tree groups per CTA: TRAV_T * TRAV_G threads share the tile
 constexpr int TRAV_ILP = RFXC_TRAV_ILP; // independent tree chains per thread
 
-template <int LAYOUT, bool SMEM_X>
+// TOP > 0 (f32 node layout): the top TOP node records (node ids < TOP — the
+// trainer numbers nodes breadth-first, so ids < 2^d - 1 cover the first d
+// levels) of the TRAV_G * TRAV_ILP trees a CTA walks per round are staged in
+// shared memory before the round, so every walk's first levels (where all
+// samples of the tile meet) are shared-memory reads; deeper levels go
+// through the read-only path.  Rounds are CTA-synchronous.
+template <int LAYOUT, bool SMEM_X, int TOP>
 __global__ void __launch_bounds__(TRAV_T * TRAV_G, 2048 / (TRAV_T * TRAV_G))
 traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ node_off,
                 int fb, int p, int tree_lo, int tree_hi, int trees_per_chunk,
@@ -133,6 +141,8 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
                 int32_t* __restrict__ codes_tm)
 {
     using V = typename std::conditional<LAYOUT == RFXC_NODES_F32, float, double>::type;
+    static_assert(TOP == 0 || LAYOUT == RFXC_NODES_F32, "tree tops: f32 layout only");
+    constexpr int RT = TRAV_G * TRAV_ILP;  // trees per round
     extern __shared__ __align__(16) unsigned char smem_raw[];
     V* xs = reinterpret_cast<V*>(smem_raw);
     const V* __restrict__ X = reinterpret_cast<const V*>(values_v);
@@ -142,6 +152,8 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
     const int64_t i = i0 + t;
     const bool valid = i < row_hi;
     const int stride = p + 1;  // odd row stride spreads banks
+    uint2* tops = reinterpret_cast<uint2*>(
+        smem_raw + (SMEM_X ? ((size_t)TRAV_T * stride * sizeof(V) + 15) / 16 * 16 : 0));
     if (SMEM_X) {
         // coalesced: consecutive threads read consecutive samples of feature f
         for (int f = grp; f < p; f += TRAV_G) {
@@ -152,11 +164,27 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
     }
     const int b_begin = tree_lo + blockIdx.y * trees_per_chunk;
     const int b_end = min(tree_hi, b_begin + trees_per_chunk);
-    if (!valid) return;
+    if (TOP == 0 && !valid) return;
     const uint32_t fmask = (1u << fb) - 1u;
 
-    // group g takes trees b_begin + g*ILP + j*(G*ILP) ... (ILP consecutive trees)
-    for (int b = b_begin + grp * TRAV_ILP; b < b_end; b += TRAV_G * TRAV_ILP) {
+    // round j: trees b_begin + j*RT + [0, RT); group g takes its ILP
+    // consecutive trees of the round
+    for (int b0 = b_begin; b0 < b_end; b0 += RT) {
+        if (TOP > 0) {
+            __syncthreads();  // the previous round's walks are done with the tops
+            const uint2* nodes = reinterpret_cast<const uint2*>(nodes_v);
+            for (int e = threadIdx.x; e < RT * TOP; e += TRAV_T * TRAV_G) {
+                const int slot = e / TOP, id = e % TOP;
+                const int tb = b0 + slot;
+                if (tb < b_end) {
+                    const int64_t o = node_off[tb];
+                    if (o + id < node_off[tb + 1]) tops[e] = __ldg(nodes + o + id);
+                }
+            }
+            __syncthreads();
+            if (!valid) continue;
+        }
+        const int b = b0 + grp * TRAV_ILP;
         int64_t base[TRAV_ILP];
         uint32_t id[TRAV_ILP];
         int32_t code[TRAV_ILP];
@@ -175,7 +203,9 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
             for (int c = 0; c < TRAV_ILP; c++) {
                 if (!act[c]) continue;
                 if (LAYOUT == RFXC_NODES_F32) {
-                    uint2 nd = __ldg(reinterpret_cast<const uint2*>(nodes_v) + base[c] + id[c]);
+                    const uint2 nd = (TOP > 0 && id[c] < (uint32_t)TOP)
+                                         ? tops[(grp * TRAV_ILP + c) * TOP + id[c]]
+                                         : __ldg(reinterpret_cast<const uint2*>(nodes_v) + base[c] + id[c]);
                     if (nd.y == 0u) {
                         code[c] = (int32_t)nd.x;
                         act[c] = false;
@@ -275,12 +305,13 @@ extern "C" int rfxc_forest_pack(const int8_t* d_status, const int32_t* d_split_v
     return check_launch("forest_pack");
 }
 
-template <int LAYOUT, bool SMEM_X>
+template <int LAYOUT, bool SMEM_X, int TOP>
 static int launch_traverse(const void* d_nodes, const int64_t* d_node_off, int p, int tree_lo,
                            int tree_hi, const void* d_values, int64_t n, int64_t row_lo,
                            int64_t row_hi, int32_t* d_codes_tm, size_t smem, cudaStream_t st)
 {
-    auto kern = traverse_kernel<LAYOUT, SMEM_X>;
+    auto kern = traverse_kernel<LAYOUT, SMEM_X, TOP>;
+    if (TOP > 0) smem = (smem + 15) / 16 * 16 + (size_t)TRAV_G * TRAV_ILP * TOP * 8;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
@@ -307,6 +338,20 @@ static int launch_traverse(const void* d_nodes, const int64_t* d_node_off, int p
     return check_launch("leaf_codes");
 }
 
+// Tree-top staging (RFXC_TRAV_TOP = node records per tree in shared memory,
+// 0 = off): see traverse_kernel.  Off by default — measured slower on B200
+// (DESIGN.md §7): the tree tops are L1-resident already.
+static int trav_top()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("RFXC_TRAV_TOP");
+        v = e ? atoi(e) : 0;
+        v = v >= 255 ? 255 : v >= 127 ? 127 : v >= 63 ? 63 : 0;
+    }
+    return v;
+}
+
 extern "C" int rfxc_leaf_codes_rows(const void* d_nodes, const int64_t* d_node_off,
                                     int32_t layout, int32_t p, int32_t tree_lo, int32_t tree_hi,
                                     const void* d_values, int64_t n, int64_t row_lo,
@@ -319,13 +364,20 @@ extern "C" int rfxc_leaf_codes_rows(const void* d_nodes, const int64_t* d_node_o
     const size_t vsz = layout == RFXC_NODES_F32 ? 4 : 8;
     const size_t smem = (size_t)TRAV_T * (p + 1) * vsz;
     const bool use_smem = smem <= 112 * 1024;
-#define RFXC_TRAV(L, S) \
-    launch_traverse<L, S>(d_nodes, d_node_off, p, tree_lo, tree_hi, d_values, n, row_lo, row_hi, \
-                          d_codes_tm, S ? smem : 0, st)
-    if (layout == RFXC_NODES_F32)
-        return use_smem ? RFXC_TRAV(RFXC_NODES_F32, true) : RFXC_TRAV(RFXC_NODES_F32, false);
+#define RFXC_TRAV(L, S, TOP) \
+    launch_traverse<L, S, TOP>(d_nodes, d_node_off, p, tree_lo, tree_hi, d_values, n, row_lo, \
+                               row_hi, d_codes_tm, S ? smem : 0, st)
+    if (layout == RFXC_NODES_F32 && use_smem) {
+        switch (trav_top()) {
+            case 255: return RFXC_TRAV(RFXC_NODES_F32, true, 255);
+            case 127: return RFXC_TRAV(RFXC_NODES_F32, true, 127);
+            case 63: return RFXC_TRAV(RFXC_NODES_F32, true, 63);
+            default: return RFXC_TRAV(RFXC_NODES_F32, true, 0);
+        }
+    }
+    if (layout == RFXC_NODES_F32) return RFXC_TRAV(RFXC_NODES_F32, false, 0);
     if (layout == RFXC_NODES_F64)
-        return use_smem ? RFXC_TRAV(RFXC_NODES_F64, true) : RFXC_TRAV(RFXC_NODES_F64, false);
+        return use_smem ? RFXC_TRAV(RFXC_NODES_F64, true, 0) : RFXC_TRAV(RFXC_NODES_F64, false, 0);
 #undef RFXC_TRAV
     return fail(RFXC_EDATA, "leaf_codes: unknown layout %d", layout);
 }

@@ -374,15 +374,18 @@ gram_stage_kernel(const double* __restrict__ A, const double* __restrict__ Bm, i
     const int GA = 8 * TA, GB = 8 * TB;
     const int ca = threadIdx.x % GA, ra0 = threadIdx.x / GA, rsa = (int)blockDim.x / GA;
     const int cb = threadIdx.x % GB, rb0 = threadIdx.x / GB, rsb = (int)blockDim.x / GB;
+    // (threads beyond rsa * GA / rsb * GB copy nothing: with GA not dividing
+    // the block, their rows would repeat other threads' rows — a write-write
+    // race compute-sanitizer's racecheck reported)
     auto stage = [&](int64_t c, int buf) {
         double* sa = gss + buf * per;
-        if (ra0 < GS_CH)
+        if (ra0 < GS_CH && ra0 < rsa)
             for (int row = ra0; row < GS_CH; row += rsa) {
                 const int64_t g = c + row;
                 const bool ok = g < r1 && ca < ka;
                 cp_async8z(sa + row * lsa + ca, ok ? A + g * ka + ca : A, ok);
             }
-        if (!sym && rb0 < GS_CH) {
+        if (!sym && rb0 < GS_CH && rb0 < rsb) {
             double* sb = sa + GS_CH * lsa;
             for (int row = rb0; row < GS_CH; row += rsb) {
                 const int64_t g = c + row;
@@ -400,12 +403,15 @@ gram_stage_kernel(const double* __restrict__ A, const double* __restrict__ Bm, i
     }
     int bl = nst - 1, bu = 0;  // buffer to load into / to use
     for (int it = 0; it < nch; it++) {
+        // chunk it has landed (this thread's copies; the barrier makes every
+        // thread's visible) and every warp is done with chunk it - 1, whose
+        // buffer the next stage overwrites (compute-sanitizer racecheck)
+        cp_async_wait_dyn(nst - 2);
+        __syncthreads();
         const int nx = it + nst - 1;
         if (nx < nch) stage(r0 + (int64_t)nx * GS_CH, bl);
         else cp_async_commit();
         bl = bl + 1 == nst ? 0 : bl + 1;
-        cp_async_wait_dyn(nst - 1);
-        __syncthreads();
         const double* sa = gss + bu * per;
         const double* sb = sym ? sa : sa + GS_CH * lsa;
         bu = bu + 1 == nst ? 0 : bu + 1;
@@ -417,7 +423,6 @@ gram_stage_kernel(const double* __restrict__ A, const double* __restrict__ Bm, i
             for (int m = 0; m < MT; m++)
                 if (tb[m] >= 0) dmma884(acc[m][0], acc[m][1], ra[8 * ta[m]], rb[8 * tb[m]]);
         }
-        __syncthreads();
     }
     double* out = parts + (int64_t)blockIdx.x * ka * kb;
 #pragma unroll

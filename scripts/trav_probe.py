@@ -1,30 +1,36 @@
-"""Time K1 traversal (rfxc_leaf_codes) on the bench-shaped forest subset."""
-import sys, time
+"""Time K1 traversal (rfxc_leaf_codes) on a bench-shaped forest subset:
+    python scripts/trav_probe.py TREES N P [NTREE_TOTAL]
+prints the traversal time per call and the SHA-256 of the codes (so tree-top
+staging variants, RFXC_TRAV_TOP=63/127/255, can be checked for equality)."""
+import hashlib
+import sys
+
 sys.path.insert(0, ".")
-import torch
-from paper_2511_19493_b200.dataset import from_arrays, make_synthetic
-from oracle.trainer import train
-from paper_2511_19493_b200.forest import TrainConfig
-from paper_2511_19493_b200.device import DeviceForest, DeviceValues, traverse, DeviceMembership
+import torch  # noqa: E402
+
+from oracle.trainer import train  # noqa: E402
+from paper_2511_19493_b200.dataset import from_arrays, make_synthetic  # noqa: E402
+from paper_2511_19493_b200.device import DeviceForest, DeviceValues, traverse  # noqa: E402
+from paper_2511_19493_b200.forest import TrainConfig  # noqa: E402
+
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000
-X, y = make_synthetic(N, 100, seed=0)
+P = int(sys.argv[3]) if len(sys.argv) > 3 else 100
+BT = int(sys.argv[4]) if len(sys.argv) > 4 else 500
+X, y = make_synthetic(N, P, seed=0)
 ds = from_arrays(X, y)
-forest = train(ds, TrainConfig(ntree=500, iseed=1), trees=(0, B))
+forest = train(ds, TrainConfig(ntree=BT, iseed=1), trees=(0, B))
 dv = DeviceValues(ds.values)
 df = DeviceForest(forest, 0, B)
 for _ in range(3):
     nb, tm, chunks = traverse(df, dv)
-    DeviceMembership(nb, tm, df.leaf_counts, 0, B, B, chunks).buckets()
 torch.cuda.synchronize()
-ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record()
 for _ in range(5):
     nb, tm, chunks = traverse(df, dv)
 ev[1].record()
-for _ in range(5):
-    DeviceMembership(nb, tm, df.leaf_counts, 0, B, B, chunks).buckets()
-ev[2].record()
 torch.cuda.synchronize()
-print(f"traverse {ev[0].elapsed_time(ev[1]) / 5:.3f} ms  bucket {ev[1].elapsed_time(ev[2]) / 5:.3f} ms  "
-      f"(n={N}, trees={B})", flush=True)
+sha = hashlib.sha256(tm.cpu().numpy().tobytes()).hexdigest()[:16]
+print(f"traverse {ev[0].elapsed_time(ev[1]) / 5:.3f} ms  (n={N}, p={P}, trees={B}) codes {sha}",
+      flush=True)
