@@ -34,3 +34,23 @@ torch.cuda.synchronize()
 sha = hashlib.sha256(tm.cpu().numpy().tobytes()).hexdigest()[:16]
 print(f"traverse {ev[0].elapsed_time(ev[1]) / 5:.3f} ms  (n={N}, p={P}, trees={B}) codes {sha}",
       flush=True)
+
+if len(sys.argv) > 5 and sys.argv[5] == "sorted":
+    # the same traversal with the samples reordered by their leaf in tree 0
+    # (neighbouring lanes then share most of their paths)
+    import numpy as np
+    from paper_2511_19493_b200.dataset import from_arrays as fa
+    order = np.argsort(tm[0].cpu().numpy(), kind="stable")
+    ds2 = fa(np.ascontiguousarray(X[order]), y[order])
+    dv2 = DeviceValues(ds2.values)
+    for _ in range(3):
+        traverse(df, dv2)
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(5):
+        nb2, tm2, _c = traverse(df, dv2)
+    ev[1].record()
+    torch.cuda.synchronize()
+    same = bool((tm2.cpu().numpy() == tm.cpu().numpy()[:, order]).all())
+    print(f"sorted by tree-0 leaf: traverse {ev[0].elapsed_time(ev[1]) / 5:.3f} ms, codes permuted "
+          f"equal: {same}", flush=True)
