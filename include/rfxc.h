@@ -180,19 +180,22 @@ int rfxc_pair_counts(const int32_t* d_codes_nb, int64_t n, int32_t B,
  * and tree b, the members that follow i in its leaf's run of d_perm.
  * d_pos_nb (n x B) uint32: absolute index of sample i in d_perm for tree b
  * (rfxc_perm_positions, then rfxc_transpose_i32); d_codes_nb / d_seg /
- * d_leaf_base as for the sketch give the end of i's run.  Work ~ n*B + same-leaf
+ * d_leaf_base as for the sketch give the end of i's run.  d_perm: the K2 perm
+ * (idx_bytes 4) or its 16-bit sample ids (idx_bytes 2, n <= 65536, from
+ * rfxc_perm_positions).  Work ~ n*B + same-leaf
  * pairs instead of n^2*B/2; the host picks it when the same-leaf pairs
  * (rfxc_same_leaf_pairs) are a small fraction of n(n-1)/2*B.  B <= 4096.
  * Same layouts and output as rfxc_pair_counts. */
-int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const uint32_t* d_perm,
+int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const void* d_perm, int32_t idx_bytes,
                           const int32_t* d_codes_nb, const int64_t* d_seg,
                           const int64_t* d_leaf_base, int64_t n, int32_t B,
                           int64_t row_lo, int64_t row_hi, int32_t layout,
                           void* d_out, void* stream);
 /* d_pos_tm (Bl x n) uint32: d_pos_tm[b*n + s] = index e with
- * d_perm[e] & ~RFXC_PERM_FIRST == s in tree b's row.  n*Bl < 2^32. */
+ * d_perm[e] & ~RFXC_PERM_FIRST == s in tree b's row.  n*Bl < 2^32.
+ * d_perm16 (nullable, n <= 65536): d_perm's sample ids as uint16. */
 int rfxc_perm_positions(const uint32_t* d_perm, int64_t n, int32_t Bl,
-                        uint32_t* d_pos_tm, void* stream);
+                        uint32_t* d_pos_tm, uint16_t* d_perm16, void* stream);
 /* *d_out = sum over leaves of s(s-1)/2, s = d_seg[g+1] - d_seg[g]. */
 int rfxc_same_leaf_pairs(const int64_t* d_seg, int64_t leaves, uint64_t* d_out,
                          void* stream);

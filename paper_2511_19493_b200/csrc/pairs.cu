@@ -116,15 +116,18 @@ constexpr int SEG_THREADS = 512;
 constexpr int SEG_UNROLL = 8;
 constexpr int SEG_QUOT_MAX = 4096;
 
-// pos_tm[b * n + sample] = absolute index of the sample in perm (tree b).
+// pos_tm[b * n + sample] = absolute index of the sample in perm (tree b);
+// perm16 (nullable, n <= 65536): the sample ids as 16-bit values — half the
+// bytes for the leaf walk, so the whole bucket stays L2-resident.
 __global__ void perm_inverse_kernel(const uint32_t* __restrict__ perm, int64_t total, int64_t n,
-                                    uint32_t* __restrict__ pos_tm)
+                                    uint32_t* __restrict__ pos_tm, uint16_t* __restrict__ perm16)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += stride) {
         const int64_t b = e / n;
         const uint32_t s = __ldg(perm + e) & ~RFXC_PERM_FIRST;
         pos_tm[b * n + s] = (uint32_t)e;
+        if (perm16) perm16[e] = (uint16_t)s;
     }
 }
 
@@ -164,9 +167,9 @@ __host__ __device__ __forceinline__ int64_t seg_smem_bytes(int64_t win, int32_t 
            (int64_t)(2 * B + 2) * 4;
 }
 
-template <int LAYOUT>
+template <int LAYOUT, typename IDX>
 __global__ void __launch_bounds__(SEG_THREADS, 2)
-pair_seg_kernel(const uint32_t* __restrict__ pos_nb, const uint32_t* __restrict__ perm,
+pair_seg_kernel(const uint32_t* __restrict__ pos_nb, const IDX* __restrict__ perm,
                 const int32_t* __restrict__ codes_nb, const int64_t* __restrict__ seg,
                 const int64_t* __restrict__ leaf_base, int64_t n, int32_t B, int64_t row_lo,
                 int64_t row_hi, int64_t win, void* __restrict__ out)
@@ -434,13 +437,14 @@ extern "C" int rfxc_pair_counts(const int32_t* d_codes_nb, int64_t n, int32_t B,
 }
 
 extern "C" int rfxc_perm_positions(const uint32_t* d_perm, int64_t n, int32_t Bl,
-                                   uint32_t* d_pos_tm, void* stream)
+                                   uint32_t* d_pos_tm, uint16_t* d_perm16, void* stream)
 {
+    if (d_perm16 && n > 65536) return fail(RFXC_EDATA, "perm_positions: 16-bit ids need n <= 65536");
     const int64_t total = n * (int64_t)Bl;
     if (n < 1 || Bl < 1 || total >= ((int64_t)1 << 32))
         return fail(RFXC_EDATA, "perm_positions: n*Bl = %lld outside [1, 2^32)", (long long)total);
     const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 16);
-    perm_inverse_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_perm, total, n, d_pos_tm);
+    perm_inverse_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_perm, total, n, d_pos_tm, d_perm16);
     return check_launch("perm_positions");
 }
 
@@ -457,8 +461,8 @@ extern "C" int rfxc_same_leaf_pairs(const int64_t* d_seg, int64_t leaves, uint64
     return check_launch("same_leaf_pairs");
 }
 
-template <int LAYOUT>
-static int launch_seg(const uint32_t* pos_nb, const uint32_t* perm, const int32_t* codes_nb,
+template <int LAYOUT, typename IDX>
+static int launch_seg(const uint32_t* pos_nb, const IDX* perm, const int32_t* codes_nb,
                       const int64_t* seg, const int64_t* leaf_base, int64_t n, int32_t B,
                       int64_t row_lo, int64_t row_hi, int64_t cap, void* out, cudaStream_t st)
 {
@@ -471,15 +475,41 @@ static int launch_seg(const uint32_t* pos_nb, const uint32_t* perm, const int32_
     int64_t win = std::min<int64_t>(cap, 2 * ((budget - fixed) / 4 - 2));
     win = std::max<int64_t>(1, std::min<int64_t>(n - 1 - row_lo, win));
     const size_t smem = (size_t)seg_smem_bytes<LAYOUT>(win, B);
-    cudaError_t e = cudaFuncSetAttribute(pair_seg_kernel<LAYOUT>,
+    cudaError_t e = cudaFuncSetAttribute(pair_seg_kernel<LAYOUT, IDX>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "pair_seg smem: %s", cudaGetErrorString(e));
-    pair_seg_kernel<LAYOUT><<<(unsigned)(row_hi - row_lo), SEG_THREADS, smem, st>>>(
+    pair_seg_kernel<LAYOUT, IDX><<<(unsigned)(row_hi - row_lo), SEG_THREADS, smem, st>>>(
         pos_nb, perm, codes_nb, seg, leaf_base, n, B, row_lo, row_hi, win, out);
     return check_launch("pair_counts_leaf");
 }
 
-extern "C" int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const uint32_t* d_perm,
+template <typename IDX>
+static int pair_counts_leaf_t(const uint32_t* d_pos_nb, const IDX* d_perm, const int32_t* d_codes_nb,
+                              const int64_t* d_seg, const int64_t* d_leaf_base, int64_t n,
+                              int32_t B, int64_t row_lo, int64_t row_hi, int32_t layout,
+                              void* d_out, cudaStream_t st)
+{
+    int64_t win = INT64_MAX;  // launch_seg sizes the window to the shared memory
+    if (const char* w = getenv("RFXC_PAIRS_WINDOW")) win = std::max<int64_t>(2, atoll(w));  // tests
+    switch (layout) {
+    case RFXC_UPPER_I32:
+        return launch_seg<RFXC_UPPER_I32, IDX>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base,
+                                               n, B, row_lo, row_hi, win, d_out, st);
+    case RFXC_UPPER_F64:
+        return launch_seg<RFXC_UPPER_F64, IDX>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base,
+                                               n, B, row_lo, row_hi, win, d_out, st);
+    case RFXC_BLOCK_I32: {
+        cudaError_t e = cudaMemsetAsync(d_out, 0, (size_t)(row_hi - row_lo) * n * 4, st);
+        if (e != cudaSuccess) return fail(RFXC_ECUDA, "memset: %s", cudaGetErrorString(e));
+        return launch_seg<RFXC_BLOCK_I32, IDX>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base,
+                                               n, B, row_lo, row_hi, win, d_out, st);
+    }
+    default:
+        return fail(RFXC_EDATA, "pair_counts_leaf: unknown layout %d", layout);
+    }
+}
+
+extern "C" int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const void* d_perm, int32_t idx_bytes,
                                      const int32_t* d_codes_nb, const int64_t* d_seg,
                                      const int64_t* d_leaf_base, int64_t n, int32_t B,
                                      int64_t row_lo, int64_t row_hi, int32_t layout, void* d_out,
@@ -490,23 +520,14 @@ extern "C" int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const uint32_t* d
                     (long long)n, (long long)row_lo, (long long)row_hi);
     if (B > 4096) return fail(RFXC_EDATA, "pair_counts_leaf: B=%d > 4096 (shared per-tree tables)", B);
     if (row_hi - row_lo > 0x7fffffffLL) return fail(RFXC_EDATA, "pair_counts_leaf: rows");
+    if (idx_bytes == 2 && n > 65536) return fail(RFXC_EDATA, "pair_counts_leaf: 16-bit ids need n <= 65536");
     cudaStream_t st = as_stream(stream);
-    // counters of up to 48k columns per pass: two CTAs of 512 threads per SM
-    int64_t win = INT64_MAX;  // launch_seg sizes the window to the shared memory
-    if (const char* w = getenv("RFXC_PAIRS_WINDOW")) win = std::max<int64_t>(2, atoll(w));  // tests
-    switch (layout) {
-    case RFXC_UPPER_I32:
-        return launch_seg<RFXC_UPPER_I32>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base, n, B, row_lo, row_hi, win, d_out, st);
-    case RFXC_UPPER_F64:
-        return launch_seg<RFXC_UPPER_F64>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base, n, B, row_lo, row_hi, win, d_out, st);
-    case RFXC_BLOCK_I32: {
-        cudaError_t e = cudaMemsetAsync(d_out, 0, (size_t)(row_hi - row_lo) * n * 4, st);
-        if (e != cudaSuccess) return fail(RFXC_ECUDA, "memset: %s", cudaGetErrorString(e));
-        return launch_seg<RFXC_BLOCK_I32>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base, n, B, row_lo, row_hi, win, d_out, st);
-    }
-    default:
-        return fail(RFXC_EDATA, "pair_counts_leaf: unknown layout %d", layout);
-    }
+    if (idx_bytes == 2)
+        return pair_counts_leaf_t(d_pos_nb, static_cast<const uint16_t*>(d_perm), d_codes_nb, d_seg,
+                                  d_leaf_base, n, B, row_lo, row_hi, layout, d_out, st);
+    if (idx_bytes != 4) return fail(RFXC_EDATA, "pair_counts_leaf: idx_bytes must be 2 or 4");
+    return pair_counts_leaf_t(d_pos_nb, static_cast<const uint32_t*>(d_perm), d_codes_nb, d_seg,
+                              d_leaf_base, n, B, row_lo, row_hi, layout, d_out, st);
 }
 
 extern "C" int rfxc_triblock_count(const int32_t* d_counts_upper, int64_t n, int32_t B,

@@ -736,7 +736,13 @@ constexpr int SKP_UA = 4;
 #ifndef SKP_MINB_A
 #define SKP_MINB_A 3
 #endif   // phase A row loads in flight per lane
-constexpr int SKP_UB = 4;  // phase B row loads in flight per lane
+#ifndef SKP_UB_DEF
+#define SKP_UB_DEF 4
+#endif
+#ifndef SKP_MINB_B
+#define SKP_MINB_B 4
+#endif
+constexpr int SKP_UB = SKP_UB_DEF;  // phase B row loads in flight per lane
 
 // Phase A item: positions [P0, P1) of batch e, in steps of R sub-chunks of
 // 32 positions.  Slot s (lanes s*k4 .. s*k4+k4-1, lane c4 owning float4
@@ -1015,7 +1021,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
 // (A(0) B(0) A(1) B(1) ...), so one leaf-sum buffer suffices and each phase
 // gets its own register budget (full occupancy for the gathers).
 template <int PH, int K4>
-__global__ void __launch_bounds__(256, PH == 0 ? SKP_MINB_A : 4) sketch_phase_kernel(SkpArgs A, int e)
+__global__ void __launch_bounds__(256, PH == 0 ? SKP_MINB_A : SKP_MINB_B) sketch_phase_kernel(SkpArgs A, int e)
 {
     extern __shared__ __align__(16) uint32_t skp_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

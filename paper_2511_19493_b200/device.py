@@ -18,6 +18,7 @@ the packed bytes cross PCIe.
 
 from __future__ import annotations
 
+import os
 import weakref
 
 import numpy as np
@@ -335,6 +336,7 @@ class DeviceMembership:
         self._seg = None
         self._has_empty = None
         self._pos = None
+        self._perm16 = None
         self._pairs = None
 
     @property
@@ -375,13 +377,27 @@ class DeviceMembership:
             perm, _ = self.buckets()
             tm = torch.empty((self.Bl, self.n), dtype=torch.int32, device=perm.device)
             nb = torch.empty((self.n, self.Bl), dtype=torch.int32, device=perm.device)
+            # 16-bit sample ids for the walk when they fit (half the bytes: the
+            # bucket stays L2-resident); RFX_PAIRS_PERM16=0 keeps the 32-bit perm
+            p16 = None
+            if self.n <= 65536 and os.environ.get("RFX_PAIRS_PERM16", "1") != "0":
+                p16 = torch.empty((self.Bl, self.n), dtype=torch.int16, device=perm.device)
             with region("positions"):
                 _lib.call("rfxc_perm_positions", _lib.ptr(perm), self.n, self.Bl, _lib.ptr(tm),
-                          _lib.stream_handle())
+                          _lib.ptr(p16), _lib.stream_handle())
                 _lib.call("rfxc_transpose_i32", _lib.ptr(tm), self.Bl, self.n, _lib.ptr(nb),
                           _lib.stream_handle())
             self._pos = nb
+            self._perm16 = p16
         return self._pos
+
+    def walk_ids(self):
+        """(ids tensor, bytes per id) the leaf-walk pair counts read: the
+        16-bit copy from positions() when it exists, else the K2 perm."""
+        self.positions()
+        if self._perm16 is not None:
+            return self._perm16, 2
+        return self.buckets()[0], 4
 
     def same_leaf_pairs(self) -> int:
         """Sum over the local trees' leaves of s(s-1)/2 (exact integer)."""

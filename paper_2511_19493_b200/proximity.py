@@ -281,9 +281,9 @@ def pair_counts_device(membership: LeafMembership, layout: int, row_lo: int = 0,
     out = _device_empty(max(numel, 1), dt, d.codes_nb.device, "pair counts", n, B)
     if n >= 2 and row_hi > row_lo:
         if pair_kernel(d) == "leaf":
-            pos, (perm, seg) = d.positions(), d.buckets()
+            pos, (ids, idb), seg = d.positions(), d.walk_ids(), d.buckets()[1]
             with region("pair_counts"):
-                _lib.call("rfxc_pair_counts_leaf", _lib.ptr(pos), _lib.ptr(perm),
+                _lib.call("rfxc_pair_counts_leaf", _lib.ptr(pos), _lib.ptr(ids), idb,
                           _lib.ptr(d.codes_nb), _lib.ptr(seg), _lib.ptr(d.leaf_base), n, B,
                           row_lo, row_hi, layout, _lib.ptr(out), _lib.stream_handle())
         else:

@@ -12,11 +12,13 @@ from paper_2511_19493_b200 import proximity as P
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["leaf", "tile"])
+@pytest.fixture(autouse=True, params=["leaf", "leaf32", "tile"])
 def pair_kernel(request, monkeypatch):
     """Every count test runs on both K3 kernels: the leaf-segmented walk of
-    the K2 buckets and the compare tiles."""
-    monkeypatch.setenv("RFX_PAIRS_KERNEL", request.param)
+    the K2 buckets (over 16-bit sample ids, and over the 32-bit perm) and
+    the compare tiles."""
+    monkeypatch.setenv("RFX_PAIRS_KERNEL", request.param[:4])
+    monkeypatch.setenv("RFX_PAIRS_PERM16", "0" if request.param == "leaf32" else "1")
     return request.param
 
 
