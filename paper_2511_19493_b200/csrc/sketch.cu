@@ -553,7 +553,7 @@ constexpr int SKP_RMAX = 4;      // row slots per warp (lane groups of k4 lanes)
 constexpr int SKP_MAX_T = 32;
 
 struct SkpLayout {
-    int64_t S, part, cnt, ctr, item_leaf, total;
+    int64_t S, part, cnt, ctr, item_leaf, ypart, total;
 };
 
 __host__ __device__ inline int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
@@ -577,6 +577,7 @@ __host__ __device__ inline SkpLayout skp_layout(int64_t n, int Bl, int T, int ld
     L.cnt = off;       off += align256(s_rows * 4);
     L.ctr = off;       off += align256(2 * (int64_t)(nb + 1) * 4);
     L.item_leaf = off; off += align256(nb * ipb * 4);
+    L.ypart = off;     off += align256((int64_t)nb * n * ld * 4);  // per-batch f32 sums of phase B
     L.total = off;
     return L;
 }
@@ -589,6 +590,7 @@ struct SkpArgs {
     const int32_t* has_empty;
     const float* X;            // (n, ld)
     double* Y;                 // (n, k)
+    float* P;                  // nbatch x n x ld: phase B's f32 batch sums (null: Y read-modify-write)
     float* S;                  // 2 x s_rows x ld
     double* part;              // ipb x 2 x k
     int32_t* cnt;              // s_rows
@@ -973,7 +975,7 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
         double* y = A.Y + i * A.k + 4 * c4;
         // k = 4 * k4: the lane's 4 doubles are 32-byte aligned -> two 16-byte accesses
         const bool vec = K4 != 0 && A.k == 4 * k4;
-        if (act && !first) {
+        if (act && !first && !A.P) {
             if (vec) {
                 const double2 lo = __ldcs(reinterpret_cast<const double2*>(y));
                 const double2 hi = __ldcs(reinterpret_cast<const double2*>(y) + 1);
@@ -995,7 +997,11 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
 #pragma unroll
             for (int u = 0; u < SKP_UB; u++) f4add(acc, x[u]);
         }
-        if (act) {
+        if (act && A.P) {
+            // the batch's f32 sum leaves once (16 B per lane); the f64 sum over
+            // the batches (in batch order, identical bits) is skp_final_kernel's
+            __stcs(reinterpret_cast<float4*>(A.P + ((int64_t)e * A.n + i) * A.ld) + c4, acc);
+        } else if (act) {
             const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
             double v[4];
 #pragma unroll
@@ -1034,6 +1040,22 @@ __global__ void __launch_bounds__(256, PH == 0 ? SKP_MINB_A : SKP_MINB_B) sketch
     } else {
         const int64_t nB = (A.n + A.spw - 1) / A.spw;
         if (q < nB) skp_phase_b<K4>(A, e, q, scratch, lane);
+    }
+}
+
+// Y[i, c] = scale * sum_e P[e, i, c] in batch order, f64 — the same
+// additions, in the same order, as phase B's f64 read-modify-write of Y.
+__global__ void skp_final_kernel(const float* __restrict__ P, int nbatch, int64_t n, int ld, int k,
+                                 double scale, double* __restrict__ Y)
+{
+    const int64_t total = n * k;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = q / k;
+        const int c = (int)(q - i * k);
+        double v = 0.0;
+        for (int e = 0; e < nbatch; e++) v += (double)__ldcs(P + ((int64_t)e * n + i) * ld + c);
+        Y[q] = v * scale;
     }
 }
 
@@ -1307,6 +1329,13 @@ static void launch_phase(const SkpArgs& A, int e, cudaStream_t s)
 // stream forked from `st` (two leaf-sum buffers; A(e) waits for B(e - 2)
 // before overwriting its buffer), B stays on `st` in batch order (the Y
 // accumulation order is fixed) and the last B joins everything back.
+static void launch_final(const SkpArgs& A, cudaStream_t st)
+{
+    if (!A.P) return;
+    const int grid = (int)std::min<int64_t>(ceil_div(A.n * A.k, 256), (int64_t)sm_count() * 16);
+    skp_final_kernel<<<grid, 256, 0, st>>>(A.P, A.nbatch, A.n, A.ld, A.k, A.scale, A.Y);
+}
+
 static int launch_skp(SkpArgs& A, cudaStream_t st)
 {
     if (A.nbuf < 2) {
@@ -1314,6 +1343,7 @@ static int launch_skp(SkpArgs& A, cudaStream_t st)
             launch_phase<0>(A, e, st);
             launch_phase<1>(A, e, st);
         }
+        launch_final(A, st);
         return check_launch("sketch_pass");
     }
     static cudaStream_t aux[64] = {};
@@ -1338,6 +1368,7 @@ static int launch_skp(SkpArgs& A, cudaStream_t st)
         launch_phase<1>(A, e, st);
         cudaEventRecord(ev[2 + 2 * e], st);
     }
+    launch_final(A, st);
     return check_launch("sketch_pass");
 }
 
@@ -1364,6 +1395,12 @@ extern "C" int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg,
     A.has_empty = d_has_empty;
     A.X = d_X;
     A.Y = d_Y;
+    // per-batch f32 partials + one ordered f64 sum (no per-batch f64 Y
+    // read-modify-write); RFXC_SKETCH_YPART=0 restores the RMW
+    {
+        const char* yp = getenv("RFXC_SKETCH_YPART");
+        A.P = (yp && yp[0] == '0') ? nullptr : reinterpret_cast<float*>(w + L.ypart);
+    }
     A.S = reinterpret_cast<float*>(w + L.S);
     A.part = reinterpret_cast<double*>(w + L.part);
     A.cnt = reinterpret_cast<int32_t*>(w + L.cnt);
