@@ -173,7 +173,7 @@ int rfxc_bucket_trees(const int32_t* d_codes_tm, int64_t n, int32_t Bl,
  * (proximity.py:59-61) relative to d_out. */
 int rfxc_pair_counts(const int32_t* d_codes_nb, int64_t n, int32_t B,
                      int64_t row_lo, int64_t row_hi, int32_t layout,
-                     void* d_out, void* stream);
+                     void* d_out, const int32_t* d_gate, void* stream);
 
 /* The same counts from the K2 buckets (the reference's per-leaf pair
  * formulation, accumulate_pair_counts _kernels.py:491-510): for every row i
@@ -190,7 +190,14 @@ int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const void* d_perm, int32_t 
                           const int32_t* d_codes_nb, const int64_t* d_seg,
                           const int64_t* d_leaf_base, int64_t n, int32_t B,
                           int64_t row_lo, int64_t row_hi, int32_t layout,
-                          void* d_out, void* stream);
+                          void* d_out, const int32_t* d_gate, void* stream);
+/* d_gate (nullable, both K3 entry points, packed layouts only): the
+ * device-side choice written by rfxc_pair_kernel_gate — rfxc_pair_counts
+ * runs only if *d_gate == 0, rfxc_pair_counts_leaf only if *d_gate == 1, so
+ * the host launches both and never waits for the choice.
+ * rfxc_pair_kernel_gate: *d_gate = (*d_pairs <= share * n(n-1)/2 * B). */
+int rfxc_pair_kernel_gate(const uint64_t* d_pairs, int64_t n, int32_t B, double share,
+                          int32_t* d_gate, void* stream);
 /* d_pos_tm (Bl x n) uint32: d_pos_tm[b*n + s] = index e with
  * d_perm[e] & ~RFXC_PERM_FIRST == s in tree b's row.  n*Bl < 2^32.
  * d_perm16 (nullable, n <= 65536): d_perm's sample ids as uint16. */

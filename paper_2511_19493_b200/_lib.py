@@ -49,8 +49,9 @@ SIGNATURES = {
     "rfxc_outlier_lowrank": (ctypes.c_int, [P, I64, I32, F64, P, P]),
     "rfxc_bucket": (ctypes.c_int, [P, I64, I32, P, I32, P, P, P, P, P]),
     "rfxc_bucket_trees": (ctypes.c_int, [P, I64, I32, P, I32, I32, I32, P, P, P, P, P]),
-    "rfxc_pair_counts": (ctypes.c_int, [P, I64, I32, I64, I64, I32, P, P]),
-    "rfxc_pair_counts_leaf": (ctypes.c_int, [P, P, I32, P, P, P, I64, I32, I64, I64, I32, P, P]),
+    "rfxc_pair_counts": (ctypes.c_int, [P, I64, I32, I64, I64, I32, P, P, P]),
+    "rfxc_pair_counts_leaf": (ctypes.c_int, [P, P, I32, P, P, P, I64, I32, I64, I64, I32, P, P, P]),
+    "rfxc_pair_kernel_gate": (ctypes.c_int, [P, I64, I32, F64, P, P]),
     "rfxc_perm_positions": (ctypes.c_int, [P, I64, I32, P, P, P]),
     "rfxc_same_leaf_pairs": (ctypes.c_int, [P, I64, P, P]),
     "rfxc_triblock_count": (ctypes.c_int, [P, I64, I32, I64, I64, F64, P, P]),
@@ -129,7 +130,8 @@ LAUNCHES = {"rfxc_values_to_f32": 1, "rfxc_forest_pack": 1, "rfxc_leaf_codes": 1
             "rfxc_dequantize": 1, "rfxc_pmax": 2, "rfxc_mds_power": 1, "rfxc_gram_matvec": 1,
             "rfxc_outlier_packed": 3, "rfxc_outlier_lowrank": 1,
             "rfxc_oob_votes": 1, "rfxc_leaf_codes_rows": 1, "rfxc_pair_counts_leaf": 1,
-            "rfxc_perm_positions": 1, "rfxc_same_leaf_pairs": 1, "rfxc_pmax_draws": 1}
+            "rfxc_perm_positions": 1, "rfxc_same_leaf_pairs": 1, "rfxc_pmax_draws": 1,
+            "rfxc_pair_kernel_gate": 1}
 launch_count = 0
 
 

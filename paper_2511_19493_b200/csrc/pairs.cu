@@ -32,8 +32,9 @@ __device__ __forceinline__ int64_t row_start(int64_t i, int64_t n)
 template <int LAYOUT>
 __global__ void __launch_bounds__(PTHREADS)
 pair_tile_kernel(const int32_t* __restrict__ codes, int64_t n, int32_t B, int64_t row_lo,
-                 int64_t row_hi, void* __restrict__ out)
+                 int64_t row_hi, void* __restrict__ out, const int32_t* __restrict__ gate)
 {
+    if (gate && *gate != 0) return;  // the device chose the leaf walk
     const int64_t R = blockIdx.y, C = blockIdx.x;
     if (C < R) return;  // strictly below the diagonal band: j < i everywhere
     const int64_t i0 = row_lo + R * PT, j0 = row_lo + C * PT;
@@ -172,8 +173,10 @@ __global__ void __launch_bounds__(SEG_THREADS, 2)
 pair_seg_kernel(const uint32_t* __restrict__ pos_nb, const IDX* __restrict__ perm,
                 const int32_t* __restrict__ codes_nb, const int64_t* __restrict__ seg,
                 const int64_t* __restrict__ leaf_base, int64_t n, int32_t B, int64_t row_lo,
-                int64_t row_hi, int64_t win, void* __restrict__ out)
+                int64_t row_hi, int64_t win, void* __restrict__ out,
+                const int32_t* __restrict__ gate)
 {
+    if (gate && *gate != 1) return;  // the device chose the compare tiles
     extern __shared__ __align__(16) uint32_t cnt[];
     constexpr int NW = SEG_THREADS / 32;
     __shared__ int32_t s_wsum[NW];
@@ -283,6 +286,15 @@ pair_seg_kernel(const uint32_t* __restrict__ pos_nb, const IDX* __restrict__ per
         }
         __syncthreads();
     }
+}
+
+// gate = 1 (leaf walk) when the same-leaf pairs are at most share x units:
+// both K3 kernels are launched and the one not chosen exits at once, so the
+// choice needs no host round trip
+__global__ void pair_gate_kernel(const unsigned long long* __restrict__ pairs, double units,
+                                 double share, int32_t* __restrict__ gate)
+{
+    if (threadIdx.x == 0) *gate = ((double)*pairs <= share * units) ? 1 : 0;
 }
 
 // ---------------------------------------------------------------- TriBlock
@@ -405,7 +417,8 @@ scan_i64_kernel(const int64_t* __restrict__ in, int64_t count, int64_t* __restri
 using namespace rfxc;
 
 extern "C" int rfxc_pair_counts(const int32_t* d_codes_nb, int64_t n, int32_t B, int64_t row_lo,
-                                int64_t row_hi, int32_t layout, void* d_out, void* stream)
+                                int64_t row_hi, int32_t layout, void* d_out, const int32_t* d_gate,
+                                void* stream)
 {
     if (n < 2 || B < 1 || row_lo < 0 || row_hi > n || row_lo >= row_hi)
         return fail(RFXC_EDATA, "pair_counts: bad shape n=%lld rows=[%lld,%lld)", (long long)n,
@@ -417,17 +430,18 @@ extern "C" int rfxc_pair_counts(const int32_t* d_codes_nb, int64_t n, int32_t B,
     switch (layout) {
     case RFXC_UPPER_I32:
         pair_tile_kernel<RFXC_UPPER_I32><<<grid, PTHREADS, 0, st>>>(d_codes_nb, n, B, row_lo,
-                                                                    row_hi, d_out);
+                                                                    row_hi, d_out, d_gate);
         break;
     case RFXC_UPPER_F64:
         pair_tile_kernel<RFXC_UPPER_F64><<<grid, PTHREADS, 0, st>>>(d_codes_nb, n, B, row_lo,
-                                                                    row_hi, d_out);
+                                                                    row_hi, d_out, d_gate);
         break;
     case RFXC_BLOCK_I32: {
+        if (d_gate) return fail(RFXC_EDATA, "pair_counts: the gated launch takes packed layouts");
         cudaError_t e = cudaMemsetAsync(d_out, 0, (size_t)(row_hi - row_lo) * n * 4, st);
         if (e != cudaSuccess) return fail(RFXC_ECUDA, "memset: %s", cudaGetErrorString(e));
         pair_tile_kernel<RFXC_BLOCK_I32><<<grid, PTHREADS, 0, st>>>(d_codes_nb, n, B, row_lo,
-                                                                    row_hi, d_out);
+                                                                    row_hi, d_out, d_gate);
         break;
     }
     default:
@@ -461,10 +475,20 @@ extern "C" int rfxc_same_leaf_pairs(const int64_t* d_seg, int64_t leaves, uint64
     return check_launch("same_leaf_pairs");
 }
 
+extern "C" int rfxc_pair_kernel_gate(const uint64_t* d_pairs, int64_t n, int32_t B, double share,
+                                     int32_t* d_gate, void* stream)
+{
+    const double units = (double)n * (double)(n - 1) / 2.0 * (double)B;
+    pair_gate_kernel<<<1, 32, 0, as_stream(stream)>>>(
+        reinterpret_cast<const unsigned long long*>(d_pairs), units, share, d_gate);
+    return check_launch("pair_kernel_gate");
+}
+
 template <int LAYOUT, typename IDX>
 static int launch_seg(const uint32_t* pos_nb, const IDX* perm, const int32_t* codes_nb,
                       const int64_t* seg, const int64_t* leaf_base, int64_t n, int32_t B,
-                      int64_t row_lo, int64_t row_hi, int64_t cap, void* out, cudaStream_t st)
+                      int64_t row_lo, int64_t row_hi, int64_t cap, void* out, const int32_t* gate,
+                      cudaStream_t st)
 {
     // two CTAs per SM: the counters get what the per-tree tables leave of
     // ~100 KB (48k columns at B = 500)
@@ -479,7 +503,7 @@ static int launch_seg(const uint32_t* pos_nb, const IDX* perm, const int32_t* co
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(RFXC_ECUDA, "pair_seg smem: %s", cudaGetErrorString(e));
     pair_seg_kernel<LAYOUT, IDX><<<(unsigned)(row_hi - row_lo), SEG_THREADS, smem, st>>>(
-        pos_nb, perm, codes_nb, seg, leaf_base, n, B, row_lo, row_hi, win, out);
+        pos_nb, perm, codes_nb, seg, leaf_base, n, B, row_lo, row_hi, win, out, gate);
     return check_launch("pair_counts_leaf");
 }
 
@@ -487,22 +511,23 @@ template <typename IDX>
 static int pair_counts_leaf_t(const uint32_t* d_pos_nb, const IDX* d_perm, const int32_t* d_codes_nb,
                               const int64_t* d_seg, const int64_t* d_leaf_base, int64_t n,
                               int32_t B, int64_t row_lo, int64_t row_hi, int32_t layout,
-                              void* d_out, cudaStream_t st)
+                              void* d_out, const int32_t* gate, cudaStream_t st)
 {
     int64_t win = INT64_MAX;  // launch_seg sizes the window to the shared memory
     if (const char* w = getenv("RFXC_PAIRS_WINDOW")) win = std::max<int64_t>(2, atoll(w));  // tests
     switch (layout) {
     case RFXC_UPPER_I32:
         return launch_seg<RFXC_UPPER_I32, IDX>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base,
-                                               n, B, row_lo, row_hi, win, d_out, st);
+                                               n, B, row_lo, row_hi, win, d_out, gate, st);
     case RFXC_UPPER_F64:
         return launch_seg<RFXC_UPPER_F64, IDX>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base,
-                                               n, B, row_lo, row_hi, win, d_out, st);
+                                               n, B, row_lo, row_hi, win, d_out, gate, st);
     case RFXC_BLOCK_I32: {
+        if (gate) return fail(RFXC_EDATA, "pair_counts_leaf: the gated launch takes packed layouts");
         cudaError_t e = cudaMemsetAsync(d_out, 0, (size_t)(row_hi - row_lo) * n * 4, st);
         if (e != cudaSuccess) return fail(RFXC_ECUDA, "memset: %s", cudaGetErrorString(e));
         return launch_seg<RFXC_BLOCK_I32, IDX>(d_pos_nb, d_perm, d_codes_nb, d_seg, d_leaf_base,
-                                               n, B, row_lo, row_hi, win, d_out, st);
+                                               n, B, row_lo, row_hi, win, d_out, gate, st);
     }
     default:
         return fail(RFXC_EDATA, "pair_counts_leaf: unknown layout %d", layout);
@@ -513,7 +538,7 @@ extern "C" int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const void* d_per
                                      const int32_t* d_codes_nb, const int64_t* d_seg,
                                      const int64_t* d_leaf_base, int64_t n, int32_t B,
                                      int64_t row_lo, int64_t row_hi, int32_t layout, void* d_out,
-                                     void* stream)
+                                     const int32_t* d_gate, void* stream)
 {
     if (n < 2 || B < 1 || row_lo < 0 || row_hi > n || row_lo >= row_hi)
         return fail(RFXC_EDATA, "pair_counts_leaf: bad shape n=%lld rows=[%lld,%lld)",
@@ -524,10 +549,10 @@ extern "C" int rfxc_pair_counts_leaf(const uint32_t* d_pos_nb, const void* d_per
     cudaStream_t st = as_stream(stream);
     if (idx_bytes == 2)
         return pair_counts_leaf_t(d_pos_nb, static_cast<const uint16_t*>(d_perm), d_codes_nb, d_seg,
-                                  d_leaf_base, n, B, row_lo, row_hi, layout, d_out, st);
+                                  d_leaf_base, n, B, row_lo, row_hi, layout, d_out, d_gate, st);
     if (idx_bytes != 4) return fail(RFXC_EDATA, "pair_counts_leaf: idx_bytes must be 2 or 4");
     return pair_counts_leaf_t(d_pos_nb, static_cast<const uint32_t*>(d_perm), d_codes_nb, d_seg,
-                              d_leaf_base, n, B, row_lo, row_hi, layout, d_out, st);
+                              d_leaf_base, n, B, row_lo, row_hi, layout, d_out, d_gate, st);
 }
 
 extern "C" int rfxc_triblock_count(const int32_t* d_counts_upper, int64_t n, int32_t B,

@@ -1045,17 +1045,43 @@ __global__ void __launch_bounds__(256, PH == 0 ? SKP_MINB_A : SKP_MINB_B) sketch
 
 // Y[i, c] = scale * sum_e P[e, i, c] in batch order, f64 — the same
 // additions, in the same order, as phase B's f64 read-modify-write of Y.
+// Thread per (row, 4-column group): the nbatch float4 loads are independent.
 __global__ void skp_final_kernel(const float* __restrict__ P, int nbatch, int64_t n, int ld, int k,
                                  double scale, double* __restrict__ Y)
 {
-    const int64_t total = n * k;
+    const int k4 = ld >> 2;
+    const int64_t total = n * k4;
+    const float4* P4 = reinterpret_cast<const float4*>(P);
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
          q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = q / k;
-        const int c = (int)(q - i * k);
-        double v = 0.0;
-        for (int e = 0; e < nbatch; e++) v += (double)__ldcs(P + ((int64_t)e * n + i) * ld + c);
-        Y[q] = v * scale;
+        const int64_t i = q / k4;
+        const int c4 = (int)(q - i * k4);
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        int e = 0;
+        for (; e + 4 <= nbatch; e += 4) {
+            float4 x[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) x[u] = __ldcs(P4 + ((int64_t)(e + u) * n + i) * k4 + c4);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                v0 += (double)x[u].x;
+                v1 += (double)x[u].y;
+                v2 += (double)x[u].z;
+                v3 += (double)x[u].w;
+            }
+        }
+        for (; e < nbatch; e++) {
+            const float4 x = __ldcs(P4 + ((int64_t)e * n + i) * k4 + c4);
+            v0 += (double)x.x;
+            v1 += (double)x.y;
+            v2 += (double)x.z;
+            v3 += (double)x.w;
+        }
+        double* y = Y + i * k + 4 * c4;
+        const double v[4] = {v0, v1, v2, v3};
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (4 * c4 + u < k) y[u] = v[u] * scale;
     }
 }
 
@@ -1332,7 +1358,7 @@ static void launch_phase(const SkpArgs& A, int e, cudaStream_t s)
 static void launch_final(const SkpArgs& A, cudaStream_t st)
 {
     if (!A.P) return;
-    const int grid = (int)std::min<int64_t>(ceil_div(A.n * A.k, 256), (int64_t)sm_count() * 16);
+    const int grid = (int)std::min<int64_t>(ceil_div(A.n * (A.ld / 4), 256), (int64_t)sm_count() * 16);
     skp_final_kernel<<<grid, 256, 0, st>>>(A.P, A.nbatch, A.n, A.ld, A.k, A.scale, A.Y);
 }
 

@@ -330,7 +330,8 @@ class DeviceMembership:
         base = np.zeros(len(leaf_counts) + 1, dtype=np.int64)
         base[1:] = np.cumsum(self.leaf_counts)
         self.leaf_base_host = base
-        self.leaf_base = torch.from_numpy(base).to(codes_nb.device)
+        # pinned + non_blocking: no host wait on the queued traversal
+        self.leaf_base = torch.from_numpy(base).pin_memory().to(codes_nb.device, non_blocking=True)
         self.total_leaves = int(base[-1])
         self._perm = None
         self._seg = None
@@ -338,6 +339,7 @@ class DeviceMembership:
         self._pos = None
         self._perm16 = None
         self._pairs = None
+        self._gate = None
 
     @property
     def Bl(self) -> int:
@@ -398,6 +400,23 @@ class DeviceMembership:
         if self._perm16 is not None:
             return self._perm16, 2
         return self.buckets()[0], 4
+
+    def pair_gate(self):
+        """Device int32: 1 when the leaf-walk pair counts apply (same-leaf
+        pairs <= LEAF_KERNEL_MAX_SHARE of the (pair, tree) units), else 0;
+        computed on the device, no host read."""
+        torch = _torch()
+        if self._gate is None:
+            from .proximity import LEAF_KERNEL_MAX_SHARE
+            _, seg = self.buckets()
+            pairs = torch.empty(1, dtype=torch.int64, device=seg.device)
+            gate = torch.empty(1, dtype=torch.int32, device=seg.device)
+            _lib.call("rfxc_same_leaf_pairs", _lib.ptr(seg), self.total_leaves, _lib.ptr(pairs),
+                      _lib.stream_handle())
+            _lib.call("rfxc_pair_kernel_gate", _lib.ptr(pairs), self.n, self.Bl,
+                      float(LEAF_KERNEL_MAX_SHARE), _lib.ptr(gate), _lib.stream_handle())
+            self._gate = gate
+        return self._gate
 
     def same_leaf_pairs(self) -> int:
         """Sum over the local trees' leaves of s(s-1)/2 (exact integer)."""

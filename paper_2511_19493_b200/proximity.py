@@ -280,16 +280,30 @@ def pair_counts_device(membership: LeafMembership, layout: int, row_lo: int = 0,
     _device_budget(numel * (8 if dt == torch.float64 else 4), "pair counts", n, B)
     out = _device_empty(max(numel, 1), dt, d.codes_nb.device, "pair counts", n, B)
     if n >= 2 and row_hi > row_lo:
-        if pair_kernel(d) == "leaf":
+        choice = pair_kernel(d, decide=False)
+        if choice == "auto" and layout == _lib.BLOCK_I32:
+            choice = pair_kernel(d)  # the row-block layout is not gated (host choice)
+        if choice == "auto":
+            # both kernels launched; the device-side gate lets one of them run
+            pos, (ids, idb), seg = d.positions(), d.walk_ids(), d.buckets()[1]
+            gate = d.pair_gate()
+            with region("pair_counts"):
+                _lib.call("rfxc_pair_counts_leaf", _lib.ptr(pos), _lib.ptr(ids), idb,
+                          _lib.ptr(d.codes_nb), _lib.ptr(seg), _lib.ptr(d.leaf_base), n, B,
+                          row_lo, row_hi, layout, _lib.ptr(out), _lib.ptr(gate),
+                          _lib.stream_handle())
+                _lib.call("rfxc_pair_counts", _lib.ptr(d.codes_nb), n, B, row_lo, row_hi, layout,
+                          _lib.ptr(out), _lib.ptr(gate), _lib.stream_handle())
+        elif choice == "leaf":
             pos, (ids, idb), seg = d.positions(), d.walk_ids(), d.buckets()[1]
             with region("pair_counts"):
                 _lib.call("rfxc_pair_counts_leaf", _lib.ptr(pos), _lib.ptr(ids), idb,
                           _lib.ptr(d.codes_nb), _lib.ptr(seg), _lib.ptr(d.leaf_base), n, B,
-                          row_lo, row_hi, layout, _lib.ptr(out), _lib.stream_handle())
+                          row_lo, row_hi, layout, _lib.ptr(out), None, _lib.stream_handle())
         else:
             with region("pair_counts"):
                 _lib.call("rfxc_pair_counts", _lib.ptr(d.codes_nb), n, B, row_lo, row_hi, layout,
-                          _lib.ptr(out), _lib.stream_handle())
+                          _lib.ptr(out), None, _lib.stream_handle())
     return out[:numel]
 
 
@@ -300,14 +314,18 @@ def pair_counts_device(membership: LeafMembership, layout: int, row_lo: int = 0,
 LEAF_KERNEL_MAX_SHARE = 0.2
 
 
-def pair_kernel(d) -> str:
+def pair_kernel(d, decide: bool = True) -> str:
     """'leaf' (K2-bucket walk, the reference's per-leaf formulation) or
-    'tile' (compare tiles); RFX_PAIRS_KERNEL=leaf|tile forces one."""
+    'tile' (compare tiles); RFX_PAIRS_KERNEL=leaf|tile forces one.  With
+    decide=False the data-dependent case returns 'auto' (the device decides,
+    no host round trip)."""
     forced = os.environ.get("RFX_PAIRS_KERNEL")
     if forced in ("leaf", "tile"):
         return forced
     if d.B > 4096 or d.n * d.Bl >= (1 << 32):  # shared per-tree tables, u32 perm indices
         return "tile"
+    if not decide:
+        return "auto"
     units = d.n * (d.n - 1) // 2 * d.Bl
     return "leaf" if d.same_leaf_pairs() <= LEAF_KERNEL_MAX_SHARE * units else "tile"
 

@@ -65,5 +65,5 @@ def test_error_mapping(built):
     with pytest.raises(RfxError):
         _lib.check(_lib.RFXC_ECUDA, "x")
     # a shape error is reported before any device work
-    rc = _lib.load().rfxc_pair_counts(None, 1, 1, 0, 1, 0, None, None)
+    rc = _lib.load().rfxc_pair_counts(None, 1, 1, 0, 1, 0, None, None, None)
     assert rc == _lib.RFXC_EDATA and b"bad shape" in _lib.load().rfxc_last_error()

@@ -12,12 +12,16 @@ from paper_2511_19493_b200 import proximity as P
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["leaf", "leaf32", "tile"])
+@pytest.fixture(autouse=True, params=["auto", "leaf", "leaf32", "tile"])
 def pair_kernel(request, monkeypatch):
     """Every count test runs on both K3 kernels: the leaf-segmented walk of
-    the K2 buckets (over 16-bit sample ids, and over the 32-bit perm) and
-    the compare tiles."""
-    monkeypatch.setenv("RFX_PAIRS_KERNEL", request.param[:4])
+    the K2 buckets (over 16-bit sample ids, and over the 32-bit perm), the
+    compare tiles, and the default launch of both behind the device-side
+    gate."""
+    if request.param == "auto":
+        monkeypatch.delenv("RFX_PAIRS_KERNEL", raising=False)
+    else:
+        monkeypatch.setenv("RFX_PAIRS_KERNEL", request.param[:4])
     monkeypatch.setenv("RFX_PAIRS_PERM16", "0" if request.param == "leaf32" else "1")
     return request.param
 
@@ -249,3 +253,15 @@ def test_kernel_choice_follows_leaf_sizes(monkeypatch):
     one = P.LeafMembership(np.zeros((n, B), np.int32), np.ones(B, np.int32))
     assert P.pair_kernel(one.device()) == "tile"
     assert one.device().same_leaf_pairs() == B * n * (n - 1) // 2
+
+
+def test_device_gate_picks_the_tiles_for_one_leaf_trees(monkeypatch):
+    """Default (gated) launch on trees whose leaves hold every sample: the
+    gate selects the compare tiles, the leaf walk exits, counts are exact."""
+    monkeypatch.delenv("RFX_PAIRS_KERNEL", raising=False)
+    n, B = 700, 3
+    codes = np.zeros((n, B), np.int32)
+    mem = P.LeafMembership(codes, np.ones(B, np.int32))
+    up = P.pair_counts_device(mem, _lib.UPPER_I32).cpu().numpy()
+    assert int(mem.device().pair_gate().item()) == 0
+    assert np.all(up == B)

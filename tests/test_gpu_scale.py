@@ -68,13 +68,16 @@ def test_codes_sha(case):
     assert hashlib.sha256(mem.codes.tobytes()).hexdigest() == rec["codes_sha"]
 
 
-@pytest.mark.parametrize("kernel", ["leaf", "leaf32", "tile"])
+@pytest.mark.parametrize("kernel", ["auto", "leaf", "leaf32", "tile"])
 def test_whole_triangle_sha_sum_nonzero(case, kernel, monkeypatch):
     import torch
 
     from paper_2511_19493_b200 import _lib
     from paper_2511_19493_b200 import proximity as P
-    monkeypatch.setenv("RFX_PAIRS_KERNEL", kernel[:4])
+    if kernel == "auto":
+        monkeypatch.delenv("RFX_PAIRS_KERNEL", raising=False)
+    else:
+        monkeypatch.setenv("RFX_PAIRS_KERNEL", kernel[:4])
     monkeypatch.setenv("RFX_PAIRS_PERM16", "0" if kernel == "leaf32" else "1")
     _, rec, _, _, mem = case
     mem.device()._pos = None  # rebuild the walk ids for this setting
