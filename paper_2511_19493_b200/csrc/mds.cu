@@ -563,7 +563,10 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
                 for (int ks = 0; ks < 2; ks++) {
                     const int kr = 8 * ta + 4 * ks + fr, col = 8 * tb + fc;
                     const double sk = kr < r ? s.sc[kr] : 0.0, sc2 = col < r ? s.sc[col] : 0.0;
-                    sf[2 * pi + ks] = (sk * s.S[kr * (RP + 4) + col]) * sc2;
+                    // off-diagonal tile pairs count twice (symmetric S): the
+                    // exact factor 2 rides in the fragment
+                    const double wgt = ta == tb ? 1.0 : 2.0;
+                    sf[2 * pi + ks] = wgt * ((sk * s.S[kr * (RP + 4) + col]) * sc2);
                 }
 #pragma unroll
         for (int j = 0; j < 2 * RT; j++) {
@@ -611,10 +614,8 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
 #pragma unroll
                 for (int ta = 0; ta < RT; ta++)
 #pragma unroll
-                    for (int tb = ta; tb < RT; tb++, pi++) {
-                        const double wgt = ta == tb ? 1.0 : 2.0;
-                        ppu += wgt * (z[pi][0] * ep[2 * tb] + z[pi][1] * ep[2 * tb + 1]);
-                    }
+                    for (int tb = ta; tb < RT; tb++, pi++)
+                        ppu += z[pi][0] * ep[2 * tb] + z[pi][1] * ep[2 * tb + 1];
             }
 #pragma unroll
             for (int j = 0; j < 2 * RT; j++) pu += af[j] * tf[j];
