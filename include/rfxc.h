@@ -41,7 +41,9 @@ enum {
 
 /* Node layouts produced by rfxc_forest_pack. */
 enum { RFXC_NODES_F32 = 0, /* 8 B/node, thresholds rounded down to f32 */
-       RFXC_NODES_F64 = 1  /* 16 B/node, f64 thresholds             */ };
+       RFXC_NODES_F64 = 1, /* 16 B/node, f64 thresholds             */
+       RFXC_NODES_F32_NUMERIC = 2 /* traversal only: F32 records of a forest with
+                                     no categorical column (no category test per node) */ };
 
 /* Output layouts of rfxc_pair_counts. */
 enum { RFXC_UPPER_I32 = 0,  /* packed i<j rows [row_lo,row_hi), int32 counts      */

@@ -133,7 +133,7 @@ constexpr int TRAV_ILP = RFXC_TRAV_ILP; // independent tree chains per thread
 // shared memory before the round, so every walk's first levels (where all
 // samples of the tile meet) are shared-memory reads; deeper levels go
 // through the read-only path.  Rounds are CTA-synchronous.
-template <int LAYOUT, bool SMEM_X, int TOP>
+template <int LAYOUT, bool SMEM_X, int TOP, bool NUMERIC = false>
 __global__ void __launch_bounds__(TRAV_T * TRAV_G, 2048 / (TRAV_T * TRAV_G))
 traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ node_off,
                 int fb, int p, int tree_lo, int tree_hi, int trees_per_chunk,
@@ -215,7 +215,7 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
                     const float v = SMEM_X ? (float)xs[t * stride + f]
                                            : (float)X[(int64_t)f * n + i];
                     bool go;
-                    if ((nd.y >> fb) & 1u) {
+                    if (!NUMERIC && ((nd.y >> fb) & 1u)) {
                         uint32_t lv = (uint32_t)(int)v;
                         go = lv < 32u ? ((nd.x >> lv) & 1u) : false;
                     } else {
@@ -305,12 +305,12 @@ extern "C" int rfxc_forest_pack(const int8_t* d_status, const int32_t* d_split_v
     return check_launch("forest_pack");
 }
 
-template <int LAYOUT, bool SMEM_X, int TOP>
+template <int LAYOUT, bool SMEM_X, int TOP, bool NUMERIC = false>
 static int launch_traverse(const void* d_nodes, const int64_t* d_node_off, int p, int tree_lo,
                            int tree_hi, const void* d_values, int64_t n, int64_t row_lo,
                            int64_t row_hi, int32_t* d_codes_tm, size_t smem, cudaStream_t st)
 {
-    auto kern = traverse_kernel<LAYOUT, SMEM_X, TOP>;
+    auto kern = traverse_kernel<LAYOUT, SMEM_X, TOP, NUMERIC>;
     if (TOP > 0) smem = (smem + 15) / 16 * 16 + (size_t)TRAV_G * TRAV_ILP * TOP * 8;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -361,12 +361,19 @@ extern "C" int rfxc_leaf_codes_rows(const void* d_nodes, const int64_t* d_node_o
         return fail(RFXC_EDATA, "leaf_codes: bad shape");
     if (row_lo < 0 || row_hi > n || row_lo >= row_hi) return fail(RFXC_EDATA, "leaf_codes: bad rows");
     cudaStream_t st = as_stream(stream);
-    const size_t vsz = layout == RFXC_NODES_F32 ? 4 : 8;
+    const size_t vsz = layout == RFXC_NODES_F64 ? 8 : 4;
     const size_t smem = (size_t)TRAV_T * (p + 1) * vsz;
     const bool use_smem = smem <= 112 * 1024;
 #define RFXC_TRAV(L, S, TOP) \
     launch_traverse<L, S, TOP>(d_nodes, d_node_off, p, tree_lo, tree_hi, d_values, n, row_lo, \
                                row_hi, d_codes_tm, S ? smem : 0, st)
+    if (layout == RFXC_NODES_F32_NUMERIC) {  // f32 records, no categorical split anywhere
+        if (use_smem && trav_top() == 0)
+            return launch_traverse<RFXC_NODES_F32, true, 0, true>(d_nodes, d_node_off, p, tree_lo,
+                                                                 tree_hi, d_values, n, row_lo, row_hi,
+                                                                 d_codes_tm, smem, st);
+        layout = RFXC_NODES_F32;
+    }
     if (layout == RFXC_NODES_F32 && use_smem) {
         switch (trav_top()) {
             case 255: return RFXC_TRAV(RFXC_NODES_F32, true, 255);

@@ -212,6 +212,8 @@ class DeviceForest:
         if layout == _lib.NODES_F32 and not self.f32_ok:
             raise DataError("tree too large for the 8-byte node layout")
         self.layout = layout
+        # no categorical column: the traversal skips the per-node category test
+        self.numeric = not bool(np.any(col_cat))
 
         def stage():
             keep = []  # keep converted arrays alive during the call
@@ -466,9 +468,11 @@ def traverse(dforest: DeviceForest, dvalues: DeviceValues):
     f32_rows = dvalues.rows_ready if layout == _lib.NODES_F32 else []
     done = []  # (c0, c1, event after the chunk's codes)
 
+    klayout = _lib.NODES_F32_NUMERIC if layout == _lib.NODES_F32 and dforest.numeric else layout
+
     def walk(c0, c1, lo, hi):
         _lib.call("rfxc_leaf_codes_rows", _lib.ptr(dforest._nodes), _lib.ptr(dforest.node_off),
-                  layout, dvalues.p, c0, c1, _lib.ptr(vals), n, lo, hi, _lib.ptr(tm[c0:c1]),
+                  klayout, dvalues.p, c0, c1, _lib.ptr(vals), n, lo, hi, _lib.ptr(tm[c0:c1]),
                   _lib.stream_handle())
 
     def mark(c0, c1):
