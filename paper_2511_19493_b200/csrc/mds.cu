@@ -46,7 +46,10 @@ constexpr int BS = 24;         // reduction-B slots
 constexpr int MAXRT = 24;      // r <= 192
 constexpr int SMS_MAXRP = 96;  // S kept in shared memory up to RP = 96
 constexpr int SMEM_BUDGET = 222 * 1024;  // + ~3 KB of static shared memory
-constexpr int MDS_I8F_THREADS = 256;     // int8-resident fast path (r <= 32)
+#ifndef RFXC_MDS_I8F_THREADS
+#define RFXC_MDS_I8F_THREADS 256
+#endif
+constexpr int MDS_I8F_THREADS = RFXC_MDS_I8F_THREADS;  // int8-resident fast path (r <= 32)
 
 enum { QS_F64 = 0, QS_I8 = 1, QS_GLOBAL = 2 };
 
@@ -597,26 +600,26 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
                 const int w = fr >= 2 ? wv[(j & ~1) + 1] : wv[j & ~1];
                 ep[j] = (double)(int8_t)(w >> (8 * ((2 * fr + (j & 1)) & 3)));
             }
-            double z[NPF][2];
+            // z_tb = sum over ta <= tb of the row's codes (tile ta) times S~(ta, tb):
+            // one accumulator per column tile, the tile pairs and k-steps
+            // accumulated on the tensor core (pairs ordered ks-major so the
+            // chains interleave across tiles)
+            double z[RT][2];
 #pragma unroll
-            for (int pi = 0; pi < NPF; pi++) z[pi][0] = z[pi][1] = 0.0;
+            for (int tb = 0; tb < RT; tb++) z[tb][0] = z[tb][1] = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < 2; ks++) {
-                int pi = 0;
+            for (int ta = 0; ta < RT; ta++)
 #pragma unroll
-                for (int ta = 0; ta < RT; ta++)
+                for (int ks = 0; ks < 2; ks++) {
 #pragma unroll
-                    for (int tb = ta; tb < RT; tb++, pi++)
-                        dmma884(z[pi][0], z[pi][1], af[2 * ta + ks], sf[2 * pi + ks]);
-            }
-            {
-                int pi = 0;
+                    for (int tb = ta; tb < RT; tb++) {
+                        const int pi = ta * RT - ta * (ta - 1) / 2 + (tb - ta);
+                        dmma884(z[tb][0], z[tb][1], af[2 * ta + ks], sf[2 * pi + ks]);
+                    }
+                }
 #pragma unroll
-                for (int ta = 0; ta < RT; ta++)
-#pragma unroll
-                    for (int tb = ta; tb < RT; tb++, pi++)
-                        ppu += z[pi][0] * ep[2 * tb] + z[pi][1] * ep[2 * tb + 1];
-            }
+            for (int tb = 0; tb < RT; tb++)
+                ppu += z[tb][0] * ep[2 * tb] + z[tb][1] * ep[2 * tb + 1];
 #pragma unroll
             for (int j = 0; j < 2 * RT; j++) pu += af[j] * tf[j];
         } else if constexpr (QS == QS_F64 && SMS) {
