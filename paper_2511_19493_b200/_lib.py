@@ -141,9 +141,9 @@ def call(name: str, *args) -> None:
     launch_count += LAUNCHES.get(name, 0)
     if name == "rfxc_mds_power":
         launch_count += int(args[7])  # start-vector normals, one per component
-    elif name == "rfxc_sketch_pass":  # a leaf-sum and a gather kernel per tree batch
+    elif name == "rfxc_sketch_pass":  # a leaf-sum and a gather kernel per tree batch + the sum
         Bl, T = int(args[6]), int(args[11])
-        launch_count += 2 * ((Bl + T - 1) // T) - 1
+        launch_count += 2 * ((Bl + T - 1) // T)
     elif name in ("rfxc_bucket", "rfxc_bucket_trees"):  # launches of <= 2 trees per SM
         trees = int(args[2]) if name == "rfxc_bucket" else int(args[6]) - int(args[5])
         launch_count += max(0, (trees + 2 * _sms() - 1) // (2 * _sms()) - 1)

@@ -5,8 +5,10 @@ import csv
 import sys
 
 path = sys.argv[1]
-steps = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 rows = [r for r in csv.reader(open(path)) if len(r) > 10 and r[0].isdigit()]
+# steps: the given count, or "mds" = the number of MDS launches (one per step)
+arg = sys.argv[2] if len(sys.argv) > 2 else "1"
+steps = float(sum(1 for r in rows if "mds_kernel" in r[4])) if arg == "mds" else float(arg)
 d = collections.defaultdict(list)
 for r in rows:
     name = r[4].split("(")[0].split("<")[0].replace("void ", "")

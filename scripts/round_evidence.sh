@@ -10,7 +10,7 @@ NOCOMPAT=1 bash scripts/gpu_refsuite.sh > /dev/null 2>&1; tail -14 gpurun_out/re
 timeout 1200 python bench.py --steps ${STEPS:-20} --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
 timeout 1500 python bench.py --impl reference --steps ${REFSTEPS:-3} --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -1 gpurun_out/bench_ref.json | cut -c1-300
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-secondary > gpurun_out/ncu_bench.out 2>&1
-python scripts/launch_summary.py gpurun_out/launches.csv 8 > gpurun_out/launches_summary.txt 2>&1; head -16 gpurun_out/launches_summary.txt
+python scripts/launch_summary.py gpurun_out/launches.csv mds > gpurun_out/launches_summary.txt 2>&1; head -16 gpurun_out/launches_summary.txt
 if [ -z "$NOFULL" ]; then
 for k in ${KERNELS:-sketch_phase_kernel mds_kernel traverse_kernel radix_bucket_kernel}; do
   c=1; if [ $k = sketch_phase_kernel ]; then c=2; fi
