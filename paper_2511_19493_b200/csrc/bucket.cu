@@ -27,7 +27,10 @@ namespace rfxc {
 // the per-CTA scratch pair.
 constexpr int RB_MAXPASS = 4;
 constexpr int RB_W = 16;  // warps per CTA
-constexpr int RB_U = 8;   // 32-element steps per warp per tile
+#ifndef RFXC_RB_U
+#define RFXC_RB_U 8
+#endif
+constexpr int RB_U = RFXC_RB_U;  // 32-element steps per warp per tile
 
 template <int W, int U>
 struct RbSmem {
