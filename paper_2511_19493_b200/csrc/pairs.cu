@@ -250,25 +250,41 @@ pair_seg_kernel(const uint32_t* __restrict__ pos_nb, const IDX* __restrict__ per
             }
             t = lo;
         }
-        for (int32_t e0 = e_lo + lane; e0 < e_hi; e0 += 32 * SEG_UNROLL) {
+        // the current tree's end and base stay in registers; reloaded only
+        // when the lane's entry crosses into the next tree
+        int32_t tend = s_end[t + 1];
+        uint32_t tbase = s_base[t];
+        // full groups of SEG_UNROLL lane steps (no bounds checks), then the tail
+        int32_t e0 = e_lo + lane;
+        const int32_t e_full = e_hi - 32 * (SEG_UNROLL - 1);  // e0 < e_full: the whole group fits
+        for (; e0 < e_full; e0 += 32 * SEG_UNROLL) {
             uint32_t v[SEG_UNROLL];
 #pragma unroll
             for (int u = 0; u < SEG_UNROLL; u++) {
                 const int32_t e = e0 + u * 32;
-                v[u] = 0xffffffffu;
-                if (e < e_hi) {
-                    while (s_end[t + 1] <= e) t++;
-                    v[u] = __ldg(perm + (uint32_t)(s_base[t] + (uint32_t)e));
+                while (tend <= e) {
+                    t++;
+                    tend = s_end[t + 1];
+                    tbase = s_base[t];
                 }
+                v[u] = (uint32_t)__ldg(perm + (uint32_t)(tbase + (uint32_t)e));
             }
 #pragma unroll
             for (int u = 0; u < SEG_UNROLL; u++) {
-                // column offset in the window; one unsigned compare covers both
-                // ends (and the 0xffffffff no-entry sentinel)
+                // column offset in the window: one unsigned compare covers both ends
                 const uint32_t o = (v[u] & ~RFXC_PERM_FIRST) - wc0;
-                if (v[u] != 0xffffffffu && o < wlen)
-                    atomicAdd(cnt + (o >> 1), 1u << ((o & 1u) << 4));
+                if (o < wlen) atomicAdd(cnt + (o >> 1), 1u << ((o & 1u) << 4));
             }
+        }
+        for (; e0 < e_hi; e0 += 32) {
+            while (tend <= e0) {
+                t++;
+                tend = s_end[t + 1];
+                tbase = s_base[t];
+            }
+            const uint32_t v = (uint32_t)__ldg(perm + (uint32_t)(tbase + (uint32_t)e0));
+            const uint32_t o = (v & ~RFXC_PERM_FIRST) - wc0;
+            if (o < wlen) atomicAdd(cnt + (o >> 1), 1u << ((o & 1u) << 4));
         }
         __syncthreads();
         // the row leaves once, streamed past L2 (evict-first) so the perm runs
