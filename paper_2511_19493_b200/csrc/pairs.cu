@@ -114,7 +114,10 @@ pair_tile_kernel(const int32_t* __restrict__ codes, int64_t n, int32_t B, int64_
 // kernel is bound by writing the triangle, not by the counting.  Integer
 // sums: bit-exact and order-independent.
 constexpr int SEG_THREADS = 512;
-constexpr int SEG_UNROLL = 8;
+#ifndef RFXC_SEG_UNROLL
+#define RFXC_SEG_UNROLL 16
+#endif
+constexpr int SEG_UNROLL = RFXC_SEG_UNROLL;
 constexpr int SEG_QUOT_MAX = 4096;
 
 // pos_tm[b * n + sample] = absolute index of the sample in perm (tree b);

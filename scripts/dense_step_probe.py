@@ -16,7 +16,7 @@ ds, forest = bench.make_inputs(cfg, (0, cfg["B"]), os.cpu_count() or 1)
 dv = DeviceValues(ds.values)
 df = DeviceForest(forest, 0, forest.ntree)
 B = cfg["B"]
-for rep in range(6):
+for rep in range(int(os.environ.get("REPS", "6"))):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
