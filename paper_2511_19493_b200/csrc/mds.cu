@@ -347,16 +347,24 @@ __device__ void spass_i8(const MdsArgs& A, const Sm& s, int64_t rows, const doub
         const int nks = (int)(pad16(rows) >> 2);
         const int k0 = warp * nks / nw, k1 = (warp + 1) * nks / nw;
         // lane's columns 8t + fc of the zero-padded slice (codes beyond r are 0)
-        const int8_t* pq = s.q8 + fc;
+        // column 8 t + fc of row i sits at byte fc * RT + t (permuted slice)
+        const int8_t* pq = s.q8 + fc * RT;
         const int ldc = A.r8;
 #pragma unroll 2
         for (int ks = k0; ks < k1; ks++) {
             const int i = 4 * ks + fr;
             const double xq = x[i];
             double b[RT], a[RT];
+            if constexpr (RT == 4) {
+                const int wd = *reinterpret_cast<const int*>(pq + i * ldc);
+#pragma unroll
+                for (int t = 0; t < 4; t++) b[t] = (double)(int8_t)(wd >> (8 * t));
+            } else {
+#pragma unroll
+                for (int t = 0; t < RT; t++) b[t] = (double)pq[i * ldc + t];
+            }
 #pragma unroll
             for (int t = 0; t < RT; t++) {
-                b[t] = (double)pq[i * ldc + 8 * t];
                 a[t] = xq * b[t];
                 v[2 * NP + t] += a[t];
             }
@@ -588,17 +596,24 @@ __device__ void rowpass(const MdsArgs& A, const Sm& s, int64_t r0, int64_t rows,
             // the lane's 4 RT codes of the row: A-fragment columns 4 j + fr and the
             // epilogue columns 8 tb + 2 fr + h (zero-padded slice: rows to 16,
             // columns to RP), converted exactly to f64
+            // permuted slice: column c at byte (c % 8) * RT + c / 8.  A fragment j
+            // = column 4 j + fr, epilogue j = column 8 (j / 2) + 2 fr + j % 2
             const int8_t* row = s.q8 + ia * A.r8;
-            int wv[2 * RT];
-#pragma unroll
-            for (int j = 0; j < 2 * RT; j++) wv[j] = reinterpret_cast<const int*>(row)[j];
             double af[2 * RT], ep[2 * RT];
+            if constexpr (RT == 4) {
+                const int* w = reinterpret_cast<const int*>(row);
+                const int wa0 = w[fr], wa1 = w[4 + fr], we0 = w[2 * fr], we1 = w[2 * fr + 1];
 #pragma unroll
-            for (int j = 0; j < 2 * RT; j++) {
-                af[j] = (double)(int8_t)(wv[j] >> (8 * fr));
-                // column 8 tb + 2 fr + h: word 2 tb + fr / 2, byte (2 fr + h) & 3
-                const int w = fr >= 2 ? wv[(j & ~1) + 1] : wv[j & ~1];
-                ep[j] = (double)(int8_t)(w >> (8 * ((2 * fr + (j & 1)) & 3)));
+                for (int j = 0; j < 2 * RT; j++) {
+                    af[j] = (double)(int8_t)(((j & 1) ? wa1 : wa0) >> (8 * (j >> 1)));
+                    ep[j] = (double)(int8_t)(((j & 1) ? we1 : we0) >> (8 * (j >> 1)));
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 2 * RT; j++) {
+                    af[j] = (double)row[(4 * (j & 1) + fr) * RT + (j >> 1)];
+                    ep[j] = (double)row[(2 * fr + (j & 1)) * RT + (j >> 1)];
+                }
             }
             // z_tb = sum over ta <= tb of the row's codes (tile ta) times S~(ta, tb):
             // one accumulator per column tile, the tile pairs and k-steps
@@ -776,11 +791,14 @@ __global__ void __launch_bounds__(NTH, 1) mds_kernel(MdsArgs A)
     if (QS == QS_I8) {
         int8_t* q8 = reinterpret_cast<int8_t*>(scs + r);
         for (int e = threadIdx.x; e < r; e += (int)blockDim.x) scs[e] = A.scales[e];
-        // zero-padded to pad16(rpb) rows x RP columns (A.r8 = RP)
+        // zero-padded to pad16(rpb) rows x RP columns (A.r8 = RP); the fast
+        // path (RT <= 4) stores column c of a row at byte (c % 8) * RT + c / 8,
+        // so a DMMA fragment's RT codes (columns fc, fc + 8, ...) are one load
         for (int64_t e = threadIdx.x; e < pad16(A.rpb) * RP; e += (int)blockDim.x) {
             const int64_t i = e / RP;
             const int c = (int)(e % RP);
-            q8[e] = (i < rows && c < r) ? A.codes[(r0 + i) * r + c] : (int8_t)0;
+            const int at = I8F ? (c % 8) * RT + c / 8 : c;
+            q8[i * RP + at] = (i < rows && c < r) ? A.codes[(r0 + i) * r + c] : (int8_t)0;
         }
     } else if (QS == QS_F64) {  // zero-padded to pad16(rpb) rows x ldq columns
         double* q64 = scs + r;
