@@ -165,6 +165,9 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
     const int b_begin = tree_lo + blockIdx.y * trees_per_chunk;
     const int b_end = min(tree_hi, b_begin + trees_per_chunk);
     if (TOP == 0 && !valid) return;
+    const V* xrow = xs + t * stride;  // this sample's staged row
+    // its 32-bit shared-window address, so a visit's x is one LEA + LDS
+    const uint32_t xaddr = (uint32_t)__cvta_generic_to_shared(xrow);
     const uint32_t fmask = (1u << fb) - 1u;
 
     // round j: trees b_begin + j*RT + [0, RT); group g takes its ILP
@@ -186,6 +189,7 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
         }
         const int b = b0 + grp * TRAV_ILP;
         int64_t base[TRAV_ILP];
+        const uint2* nptr[TRAV_ILP];  // f32 layout: the chain's tree, so a visit is one IMAD.WIDE
         uint32_t id[TRAV_ILP];
         int32_t code[TRAV_ILP];
         bool act[TRAV_ILP];
@@ -193,6 +197,10 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
         for (int c = 0; c < TRAV_ILP; c++) {
             act[c] = (b + c) < b_end;
             base[c] = act[c] ? node_off[b + c] : 0;
+            // opaque to the optimiser, so a visit is one IMAD.WIDE off the
+            // chain's tree instead of a 64-bit (base + id) rebuilt each time
+            const uint2* np = reinterpret_cast<const uint2*>(nodes_v) + base[c];
+            asm("mov.b64 %0, %1;" : "=l"(nptr[c]) : "l"(np));
             id[c] = 0;
             code[c] = 0;
         }
@@ -205,15 +213,18 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
                 if (LAYOUT == RFXC_NODES_F32) {
                     const uint2 nd = (TOP > 0 && id[c] < (uint32_t)TOP)
                                          ? tops[(grp * TRAV_ILP + c) * TOP + id[c]]
-                                         : __ldg(reinterpret_cast<const uint2*>(nodes_v) + base[c] + id[c]);
+                                         : __ldg(nptr[c] + id[c]);
                     if (nd.y == 0u) {
                         code[c] = (int32_t)nd.x;
                         act[c] = false;
                         continue;
                     }
                     const uint32_t f = nd.y & fmask;
-                    const float v = SMEM_X ? (float)xs[t * stride + f]
-                                           : (float)X[(int64_t)f * n + i];
+                    float v;
+                    if (SMEM_X)
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xaddr + 4u * f));
+                    else
+                        v = (float)X[(int64_t)f * n + i];
                     bool go;
                     if (!NUMERIC && ((nd.y >> fb) & 1u)) {
                         uint32_t lv = (uint32_t)(int)v;
@@ -230,8 +241,7 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
                         continue;
                     }
                     const int f = nd.z & 0x3fffffff;
-                    const double v = SMEM_X ? (double)xs[t * stride + f]
-                                            : (double)X[(int64_t)f * n + i];
+                    const double v = SMEM_X ? (double)xrow[f] : (double)X[(int64_t)f * n + i];
                     long long bits = ((long long)(unsigned)nd.y << 32) | (unsigned)nd.x;
                     bool go;
                     if (nd.z & (1 << 30)) {
