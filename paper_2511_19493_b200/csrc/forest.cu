@@ -192,11 +192,12 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
         const uint2* nptr[TRAV_ILP];  // f32 layout: the chain's tree, so a visit is one IMAD.WIDE
         uint32_t id[TRAV_ILP];
         int32_t code[TRAV_ILP];
-        bool act[TRAV_ILP];
+        uint32_t actm = 0;  // bit c: chain c still walking
 #pragma unroll
         for (int c = 0; c < TRAV_ILP; c++) {
-            act[c] = (b + c) < b_end;
-            base[c] = act[c] ? node_off[b + c] : 0;
+            const bool live = (b + c) < b_end;
+            if (live) actm |= 1u << c;
+            base[c] = live ? node_off[b + c] : 0;
             // opaque to the optimiser, so a visit is one IMAD.WIDE off the
             // chain's tree instead of a 64-bit (base + id) rebuilt each time
             const uint2* np = reinterpret_cast<const uint2*>(nodes_v) + base[c];
@@ -204,19 +205,17 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
             id[c] = 0;
             code[c] = 0;
         }
-        bool any = true;
-        while (any) {
-            any = false;
+        while (actm) {
 #pragma unroll
             for (int c = 0; c < TRAV_ILP; c++) {
-                if (!act[c]) continue;
+                if (!(actm & (1u << c))) continue;
                 if (LAYOUT == RFXC_NODES_F32) {
                     const uint2 nd = (TOP > 0 && id[c] < (uint32_t)TOP)
                                          ? tops[(grp * TRAV_ILP + c) * TOP + id[c]]
                                          : __ldg(nptr[c] + id[c]);
                     if (nd.y == 0u) {
                         code[c] = (int32_t)nd.x;
-                        act[c] = false;
+                        actm &= ~(1u << c);
                         continue;
                     }
                     const uint32_t f = nd.y & fmask;
@@ -237,7 +236,7 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
                     int4 nd = __ldg(reinterpret_cast<const int4*>(nodes_v) + base[c] + id[c]);
                     if (nd.z < 0) {
                         code[c] = nd.w;
-                        act[c] = false;
+                        actm &= ~(1u << c);
                         continue;
                     }
                     const int f = nd.z & 0x3fffffff;
@@ -252,7 +251,6 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
                     }
                     id[c] = (uint32_t)nd.w + (go ? 0u : 1u);
                 }
-                any = true;
             }
         }
 #pragma unroll
