@@ -735,6 +735,9 @@ __device__ __forceinline__ void slot_combine(float4& a, int R, int k4, int slot,
 constexpr int SKP_SLOT = 36;
 constexpr int SKP_SCRATCH = SKP_RMAX * SKP_SLOT + 2 * 32 * 4;  // + head/tail float4 per lane
 constexpr int SKP_UA = 4;
+#ifndef SKP_BRANCHLESS_A
+#define SKP_BRANCHLESS_A 1
+#endif
 #ifndef SKP_MINB_A
 #define SKP_MINB_A 3
 #endif   // phase A row loads in flight per lane
@@ -844,7 +847,37 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
             inside = true;
         };  // the caller restarts acc with the row at p
         static_assert(SKP_UA == 4, "index loads are uint4");
-        if (P1 - (P0 + 32 * (int64_t)s0) >= 32 * R) {
+        if (!he && P1 - (P0 + 32 * (int64_t)s0) >= 32 * R && SKP_BRANCHLESS_A) {
+            // every slot has 32 positions and leaf ids follow the flags: the
+            // leaf starts are handled without branches (the three slots of a
+            // warp meet their starts at different rows; a branch would run the
+            // flush path and the plain path one after the other)
+            bool ins = inside;
+            int cu = cur;
+#pragma unroll 2
+            for (int p0 = 0; p0 < 32; p0 += 4) {
+                const uint4 ix = *reinterpret_cast<const uint4*>(pb + p0);
+                float4 x[4];
+                x[0] = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.x << 4)));
+                x[1] = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.y << 4)));
+                x[2] = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.z << 4)));
+                x[3] = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.w << 4)));
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const bool fl = (fsx >> (p0 + u)) & 1u;
+                    if (fl && ins && on) Sb[(uint32_t)(cu - g0) * k4 + c4] = acc;
+                    if (fl && !ins) hsm[lane] = acc;
+                    cu += fl ? 1 : 0;
+                    ins = ins || fl;
+                    acc.x = fl ? x[u].x : acc.x + x[u].x;
+                    acc.y = fl ? x[u].y : acc.y + x[u].y;
+                    acc.z = fl ? x[u].z : acc.z + x[u].z;
+                    acc.w = fl ? x[u].w : acc.w + x[u].w;
+                }
+            }
+            inside = ins;
+            cur = cu;
+        } else if (P1 - (P0 + 32 * (int64_t)s0) >= 32 * R) {
             // every slot has 32 positions: no predicates (lanes past the last
             // slot re-read slot 0's rows and never store)
 #pragma unroll 2
