@@ -738,6 +738,10 @@ constexpr int SKP_UA = 4;
 #ifndef SKP_BRANCHLESS_A
 #define SKP_BRANCHLESS_A 1
 #endif
+#ifndef SKP_BL_UNROLL
+#define SKP_BL_UNROLL 2
+#endif
+constexpr int kSkpBlUnroll = SKP_BL_UNROLL;
 #ifndef SKP_MINB_A
 #define SKP_MINB_A 3
 #endif   // phase A row loads in flight per lane
@@ -848,13 +852,17 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
         };  // the caller restarts acc with the row at p
         static_assert(SKP_UA == 4, "index loads are uint4");
         if (!he && P1 - (P0 + 32 * (int64_t)s0) >= 32 * R && SKP_BRANCHLESS_A) {
-            // every slot has 32 positions and leaf ids follow the flags: the
-            // leaf starts are handled without branches (the three slots of a
-            // warp meet their starts at different rows; a branch would run the
-            // flush path and the plain path one after the other)
-            bool ins = inside;
-            int cu = cur;
-#pragma unroll 2
+            // every slot has 32 positions and leaf ids follow the flags: no
+            // branches.  Each leaf start p closes the running segment: the
+            // first one of a slot that started outside a leaf closes the head
+            // (-> shared memory), every other one the leaf at the running row
+            // offset of S.  The masks are fixed per sub-chunk, so each row
+            // costs three bit tests, the two predicated stores, the offset
+            // step and the four (predicated) adds.
+            const unsigned hm = inside ? 0u : (fsx & (0u - fsx));
+            const unsigned smk = fsx & ~hm;
+            uint32_t so = (uint32_t)(cur - g0) * k4 + c4;
+#pragma unroll kSkpBlUnroll
             for (int p0 = 0; p0 < 32; p0 += 4) {
                 const uint4 ix = *reinterpret_cast<const uint4*>(pb + p0);
                 float4 x[4];
@@ -862,21 +870,21 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
                 x[1] = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.y << 4)));
                 x[2] = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.z << 4)));
                 x[3] = __ldg(reinterpret_cast<const float4*>(xb + ((size_t)ix.w << 4)));
+                const unsigned f = fsx >> p0, sf = smk >> p0, hf = hm >> p0;
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    const bool fl = (fsx >> (p0 + u)) & 1u;
-                    if (fl && ins && on) Sb[(uint32_t)(cu - g0) * k4 + c4] = acc;
-                    if (fl && !ins) hsm[lane] = acc;
-                    cu += fl ? 1 : 0;
-                    ins = ins || fl;
+                    const bool fl = (f >> u) & 1u;
+                    if ((sf >> u) & 1u) Sb[so] = acc;
+                    if ((hf >> u) & 1u) hsm[lane] = acc;
+                    so += fl ? (uint32_t)k4 : 0u;
                     acc.x = fl ? x[u].x : acc.x + x[u].x;
                     acc.y = fl ? x[u].y : acc.y + x[u].y;
                     acc.z = fl ? x[u].z : acc.z + x[u].z;
                     acc.w = fl ? x[u].w : acc.w + x[u].w;
                 }
             }
-            inside = ins;
-            cur = cu;
+            cur += __popc(fsx);
+            inside = inside || fsx != 0u;
         } else if (P1 - (P0 + 32 * (int64_t)s0) >= 32 * R) {
             // every slot has 32 positions: no predicates (lanes past the last
             // slot re-read slot 0's rows and never store)

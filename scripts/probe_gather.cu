@@ -30,6 +30,46 @@ __global__ void gather_ldg(const float4* __restrict__ tab, const int* __restrict
     if (acc.x + acc.y + acc.z + acc.w == 1.2345f) out[0] = acc.y;
 }
 
+// (a2) 256-bit loads (LDG.E.ENL2.256, sm_100): 5 lanes per 160 B row, 6 rows
+// per warp instruction
+struct f8 { float4 lo, hi; };
+__device__ __forceinline__ f8 ldg256(const float* p)
+{
+    f8 v;
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v.lo.x), "=f"(v.lo.y), "=f"(v.lo.z), "=f"(v.lo.w), "=f"(v.hi.x), "=f"(v.hi.y),
+                   "=f"(v.hi.z), "=f"(v.hi.w)
+                 : "l"(p));
+    return v;
+}
+
+template <int U>
+__global__ void gather_ldg256(const float* __restrict__ tab, const int* __restrict__ idx, int64_t nrows_req,
+                              float* out)
+{
+    const int lane = threadIdx.x & 31;
+    const int slot = lane / 5, c8 = lane % 5;
+    const bool on = slot < 6;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    float4 acc = make_float4(0, 0, 0, 0);
+    for (int64_t base = gw * 6 * U; base < nrows_req; base += nw * 6 * U) {
+        f8 x[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t q = base + u * 6 + slot;
+            if (on && q < nrows_req) x[u] = ldg256(tab + (int64_t)idx[q] * 40 + c8 * 8);
+            else x[u].lo = x[u].hi = make_float4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            acc.x += x[u].lo.x + x[u].hi.x; acc.y += x[u].lo.y + x[u].hi.y;
+            acc.z += x[u].lo.z + x[u].hi.z; acc.w += x[u].lo.w + x[u].hi.w;
+        }
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 1.2345f) out[0] = acc.y;
+}
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 template <int STAGES, int ROWS>
@@ -189,6 +229,20 @@ int main()
         cudaEventElapsedTime(&ms, a, b);
         printf("LDG  %d CTA/SM: %.3f ms  %.2f TB/s (%s)\n", occ, ms, nreq * 160.0 / ms / 1e9,
                cudaGetErrorString(cudaGetLastError()));
+    }
+    for (int occ : {1, 2, 3, 4}) {
+        auto run = [&](auto kern, const char* nm) {
+            kern<<<sms * occ, 256>>>((const float*)tab, idx, nreq, out);
+            cudaEventRecord(a);
+            kern<<<sms * occ, 256>>>((const float*)tab, idx, nreq, out);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            cudaEventElapsedTime(&ms, a, b);
+            printf("%s %d CTA/SM: %.3f ms  %.2f TB/s (%s)\n", nm, occ, ms, nreq * 160.0 / ms / 1e9,
+                   cudaGetErrorString(cudaGetLastError()));
+        };
+        run(gather_ldg256<4>, "LDG256 U4 ");
+        run(gather_ldg256<8>, "LDG256 U8 ");
     }
     {
         constexpr int ST = 4, RW = 32;
