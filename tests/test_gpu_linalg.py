@@ -34,6 +34,51 @@ def test_sym_eig_matches_lapack(k):
     np.testing.assert_allclose(A @ V, V * w[None, :], atol=1e-10 * ref[0])
 
 
+def _chol_inv_host(G, shift_rel):
+    """The textbook loop rfxc_chol_inv restates (right-looking, unscaled rows,
+    a non-positive pivot leaves its row/column zero)."""
+    k = G.shape[0]
+    R = 0.5 * (G + G.T)
+    R = R + np.eye(k) * shift_rel * np.trace(R)
+    for j in range(k - 1):
+        d = R[j, j]
+        if d > 0:
+            R[j + 1:, j + 1:] -= np.triu(np.outer(R[j, j + 1:], R[j, j + 1:]) / d)
+    dg = np.diag(R).copy()
+    R = np.triu(R) / np.sqrt(np.where(dg > 0, dg, 1.0))[:, None]
+    R[dg <= 0, :] = 0.0
+    X = np.eye(k)
+    for m in range(k - 1, -1, -1):
+        X[m, m:] = X[m, m:] / R[m, m] if R[m, m] > 0 else 0.0
+        X[:m, m:] -= np.outer(R[:m, m], X[m, m:])
+    return X
+
+
+@pytest.mark.parametrize("k,shift,rankdef", [(1, 0.0, False), (5, 0.0, False), (40, 0.0, False),
+                                             (40, 1e-12, False), (40, 0.0, True), (64, 0.0, False),
+                                             (110, 1e-12, False)])
+def test_chol_inv_matches_host(k, shift, rankdef):
+    import torch
+    rng = np.random.default_rng(k)
+    B = rng.normal(size=(k + 3, k)) * np.logspace(0, -3, k)[None, :]
+    if rankdef and k > 4:
+        B[:, 3] = 0.0  # a zero pivot: its row and column of R^-1 stay zero
+    G = B.T @ B
+    out = torch.empty((k, k), dtype=torch.float64, device="cuda")
+    _lib.call("rfxc_chol_inv", _lib.ptr(dev(G)), k, shift, _lib.ptr(out), _lib.stream_handle())
+    X = out.cpu().numpy()
+    ref = _chol_inv_host(G, shift)
+    np.testing.assert_allclose(X, ref, rtol=1e-9, atol=1e-9 * np.abs(ref).max())
+    assert np.array_equal(np.tril(X, -1), np.zeros_like(X))
+    if not rankdef:  # R^-T G R^-1 = I (shift 0)
+        Gs = 0.5 * (G + G.T) + np.eye(k) * shift * np.trace(G)
+        np.testing.assert_allclose(X.T @ Gs @ X, np.eye(k), atol=1e-8)
+    # run to run identical
+    out2 = torch.empty_like(out)
+    _lib.call("rfxc_chol_inv", _lib.ptr(dev(G)), k, shift, _lib.ptr(out2), _lib.stream_handle())
+    assert torch.equal(out, out2)
+
+
 @pytest.mark.parametrize("deficient", [False, True])
 def test_orthonormalize_spans_and_is_orthonormal(deficient):
     rng = np.random.default_rng(3)
