@@ -26,7 +26,15 @@ namespace rfxc {
 // starts where the next one does).  Pass p>0 reads what pass p-1 wrote to
 // the per-CTA scratch pair.
 constexpr int RB_MAXPASS = 4;
-constexpr int RB_W = 16;  // warps per CTA
+#ifndef RFXC_RB_W
+#define RFXC_RB_W 16
+#endif
+#ifndef RFXC_RB_MINB
+#define RFXC_RB_MINB 2
+#endif
+constexpr int RB_W = RFXC_RB_W;  // warps per CTA
+constexpr int RB_MINB = RFXC_RB_MINB;  // resident CTAs per SM
+static_assert(RB_W >= 8, "the 256-digit scans need at least 256 threads");
 #ifndef RFXC_RB_U
 #define RFXC_RB_U 8
 #endif
@@ -226,7 +234,7 @@ using namespace rfxc;
 
 extern "C" int64_t rfxc_bucket_scratch_bytes(int64_t n, int32_t Bl)
 {
-    const int64_t chunk = std::min<int64_t>(Bl, (int64_t)sm_count() * 2);
+    const int64_t chunk = std::min<int64_t>(Bl, (int64_t)sm_count() * RB_MINB);
     return chunk * 2 * n * 8;
 }
 
@@ -245,15 +253,15 @@ extern "C" int rfxc_bucket_trees(const int32_t* d_codes_tm, int64_t n, int32_t B
     const int npass = std::max(1, (bits + 7) / 8);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(radix_bucket_kernel<RB_W, RB_U, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(radix_bucket_kernel<RB_W, RB_U, RB_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(RbSmem<RB_W, RB_U>));
         attr = true;
     }
-    const int64_t chunk = std::min<int64_t>(Bl, (int64_t)sm_count() * 2);
+    const int64_t chunk = std::min<int64_t>(Bl, (int64_t)sm_count() * RB_MINB);
     uint2* tmp = static_cast<uint2*>(d_scratch);
     for (int64_t t0 = tree_lo; t0 < tree_hi; t0 += chunk) {
         const int nb = (int)std::min<int64_t>(chunk, tree_hi - t0);
-        radix_bucket_kernel<RB_W, RB_U, 2><<<nb, RB_W * 32, sizeof(RbSmem<RB_W, RB_U>), st>>>(
+        radix_bucket_kernel<RB_W, RB_U, RB_MINB><<<nb, RB_W * 32, sizeof(RbSmem<RB_W, RB_U>), st>>>(
             d_codes_tm, n, d_leaf_base, (int)t0, Bl, npass, tmp, d_perm, d_seg, d_has_empty);
         const int rc = check_launch("bucket");
         if (rc) return rc;
