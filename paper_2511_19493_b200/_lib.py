@@ -19,7 +19,7 @@ BUILD_DIR = os.path.join(_HERE, "_build")
 LIB_PATH = os.path.join(BUILD_DIR, "librfxc.so")
 
 RFXC_OK, RFXC_EDATA, RFXC_EBUDGET, RFXC_ERUNTIME, RFXC_ECUDA = range(5)
-NODES_F32, NODES_F64, NODES_F32_NUMERIC = 0, 1, 2
+NODES_F32, NODES_F64, NODES_F32_NUMERIC, NODES_F32_B2, NODES_F32_B2_NUMERIC = 0, 1, 2, 3, 4
 UPPER_I32, UPPER_F64, BLOCK_I32 = 0, 1, 2
 Q_MODES = {"f32": 0, "f16": 1, "i8": 2, "nf4": 3}
 

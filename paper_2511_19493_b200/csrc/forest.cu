@@ -140,7 +140,8 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
                 const void* __restrict__ values_v, int64_t n, int64_t row_lo, int64_t row_hi,
                 int32_t* __restrict__ codes_tm)
 {
-    using V = typename std::conditional<LAYOUT == RFXC_NODES_F32, float, double>::type;
+    using V = typename std::conditional<LAYOUT == RFXC_NODES_F64, double, float>::type;
+    constexpr bool B2 = LAYOUT == RFXC_NODES_F32_B2;
     static_assert(TOP == 0 || LAYOUT == RFXC_NODES_F32, "tree tops: f32 layout only");
     constexpr int RT = TRAV_G * TRAV_ILP;  // trees per round
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -191,6 +192,7 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
         int64_t base[TRAV_ILP];
         const uint2* nptr[TRAV_ILP];  // f32 layout: the chain's tree, so a visit is one IMAD.WIDE
         uint32_t id[TRAV_ILP];
+        uint2 xr[TRAV_ILP];  // B2: record of the chain's current block root
         int32_t code[TRAV_ILP];
         uint32_t actm = 0;  // bit c: chain c still walking
 #pragma unroll
@@ -204,12 +206,48 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
             asm("mov.b64 %0, %1;" : "=l"(nptr[c]) : "l"(np));
             id[c] = 0;
             code[c] = 0;
+            if (B2) xr[c] = live ? __ldg(np) : make_uint2(0u, 0u);
         }
         while (actm) {
 #pragma unroll
             for (int c = 0; c < TRAV_ILP; c++) {
                 if (!(actm & (1u << c))) continue;
-                if (LAYOUT == RFXC_NODES_F32) {
+                if (B2) {
+                    // two levels per dependent load: decide at block root x,
+                    // then fetch the chosen child's record and (in the same
+                    // round trip) its children pair, decide at the child
+                    const uint2 nd = xr[c];
+                    if (nd.y == 0u) {
+                        code[c] = (int32_t)nd.x;
+                        actm &= ~(1u << c);
+                        continue;
+                    }
+                    auto decide = [&](const uint2 r) {
+                        const uint32_t f = r.y & fmask;
+                        float v;
+                        if (SMEM_X)
+                            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xaddr + 4u * f));
+                        else
+                            v = (float)X[(int64_t)f * n + i];
+                        if (!NUMERIC && ((r.y >> fb) & 1u)) {
+                            const uint32_t lv = (uint32_t)(int)v;
+                            return lv < 32u ? (bool)((r.x >> lv) & 1u) : false;
+                        }
+                        return v <= __uint_as_float(r.x);
+                    };
+                    const bool go = decide(nd);
+                    const uint32_t blk = nd.y >> (fb + 2);
+                    const uint32_t lint = (nd.y >> (fb + 1)) & 1u;
+                    const uint2 yr = __ldg(nptr[c] + blk + (go ? 0u : 1u));
+                    const uint4 pr =
+                        __ldg(reinterpret_cast<const uint4*>(nptr[c] + blk + 2u + ((!go && lint) ? 2u : 0u)));
+                    if (yr.y == 0u) {
+                        code[c] = (int32_t)yr.x;
+                        actm &= ~(1u << c);
+                        continue;
+                    }
+                    xr[c] = decide(yr) ? make_uint2(pr.x, pr.y) : make_uint2(pr.z, pr.w);
+                } else if (LAYOUT == RFXC_NODES_F32) {
                     const uint2 nd = (TOP > 0 && id[c] < (uint32_t)TOP)
                                          ? tops[(grp * TRAV_ILP + c) * TOP + id[c]]
                                          : __ldg(nptr[c] + id[c]);
@@ -375,6 +413,15 @@ extern "C" int rfxc_leaf_codes_rows(const void* d_nodes, const int64_t* d_node_o
 #define RFXC_TRAV(L, S, TOP) \
     launch_traverse<L, S, TOP>(d_nodes, d_node_off, p, tree_lo, tree_hi, d_values, n, row_lo, \
                                row_hi, d_codes_tm, S ? smem : 0, st)
+    if (layout == RFXC_NODES_F32_B2_NUMERIC)
+        return use_smem ? launch_traverse<RFXC_NODES_F32_B2, true, 0, true>(
+                              d_nodes, d_node_off, p, tree_lo, tree_hi, d_values, n, row_lo, row_hi,
+                              d_codes_tm, smem, st)
+                        : launch_traverse<RFXC_NODES_F32_B2, false, 0, true>(
+                              d_nodes, d_node_off, p, tree_lo, tree_hi, d_values, n, row_lo, row_hi,
+                              d_codes_tm, 0, st);
+    if (layout == RFXC_NODES_F32_B2)
+        return use_smem ? RFXC_TRAV(RFXC_NODES_F32_B2, true, 0) : RFXC_TRAV(RFXC_NODES_F32_B2, false, 0);
     if (layout == RFXC_NODES_F32_NUMERIC) {  // f32 records, no categorical split anywhere
         if (use_smem && trav_top() == 0)
             return launch_traverse<RFXC_NODES_F32, true, 0, true>(d_nodes, d_node_off, p, tree_lo,

@@ -86,10 +86,19 @@ extern "C" int rfxc_forest_pack_host(const void* const* status, const void* cons
         rfxc::last_error() = "forest_pack_host: bad shape";
         return RFXC_EDATA;
     }
-    h_node_off[0] = 0;
-    for (int b = 0; b < B; b++) h_node_off[b + 1] = h_node_off[b] + node_counts[b];
+    if (layout != RFXC_NODES_F32 && layout != RFXC_NODES_F64 && layout != RFXC_NODES_F32_B2) {
+        rfxc::last_error() = "forest_pack_host: unknown layout " + std::to_string(layout);
+        return RFXC_EDATA;
+    }
+    const bool b2 = layout == RFXC_NODES_F32_B2;
+    h_node_off[0] = 0;  // B2: one pad record per tree keeps every pair 16-byte aligned
+    for (int b = 0; b < B; b++) h_node_off[b + 1] = h_node_off[b] + node_counts[b] + (b2 ? 1 : 0);
+    if (b2)  // spare records the traversal may read past the last block (never used)
+        std::memset(static_cast<uint32_t*>(h_nodes) + 2 * h_node_off[B], 0, 4 * 8);
     const int fb = feature_bits(p);
-    const int64_t max_left = layout == RFXC_NODES_F32 ? (int64_t(1) << (31 - fb)) : INT32_MAX;
+    const int64_t max_left = layout == RFXC_NODES_F32 ? (int64_t(1) << (31 - fb))
+                           : b2                       ? (int64_t(1) << (30 - fb))
+                                                      : INT32_MAX;
     std::vector<std::string> errs(B);
     parallel_for(B, hw_threads(nthreads), [&](int64_t b) {
         const int64_t nc = node_counts[b];
@@ -110,7 +119,46 @@ extern "C" int rfxc_forest_pack_host(const void* const* status, const void* cons
             if (st[t] == 1) code[t] = nleaf++;
         h_leaf_counts[b] = nleaf;
         std::vector<int64_t> newid;
-        if (!adjacent) {
+        if (b2) {
+            // [root, pad] then the two-level blocks in breadth-first order of
+            // their roots; order[new] = old id (-1: pad)
+            order.reserve(nc + 1);
+            newid.assign(nc, -1);
+            order.push_back(0);
+            order.push_back(-1);
+            newid[0] = 0;
+            auto internal = [&](int64_t t) { return st[t] == 0; };
+            auto place_children = [&](int64_t o) {
+                for (int64_t ch : {(int64_t)lf[o], (int64_t)rt[o]}) {
+                    if (ch <= 0 || ch >= nc || newid[ch] >= 0) return false;
+                    newid[ch] = (int64_t)order.size();
+                    order.push_back(ch);
+                }
+                return true;
+            };
+            std::vector<int64_t> roots;
+            if (internal(0)) roots.push_back(0);
+            for (size_t q = 0; q < roots.size(); q++) {
+                const int64_t x = roots[q];
+                if (!place_children(x)) {
+                    errs[b] = "tree " + std::to_string(b) + ": malformed children";
+                    return;
+                }
+                for (int64_t y : {(int64_t)lf[x], (int64_t)rt[x]}) {
+                    if (!internal(y)) continue;
+                    if (!place_children(y)) {
+                        errs[b] = "tree " + std::to_string(b) + ": malformed children";
+                        return;
+                    }
+                    for (int64_t g : {(int64_t)lf[y], (int64_t)rt[y]})
+                        if (internal(g)) roots.push_back(g);
+                }
+            }
+            if ((int64_t)order.size() != nc + 1) {
+                errs[b] = "tree " + std::to_string(b) + ": unreachable nodes";
+                return;
+            }
+        } else if (!adjacent) {
             order.reserve(nc);
             newid.assign(nc, -1);
             order.push_back(0);
@@ -134,10 +182,16 @@ extern "C" int rfxc_forest_pack_host(const void* const* status, const void* cons
             }
         }
         const int64_t base = h_node_off[b];
-        for (int64_t t = 0; t < nc; t++) {
-            const int64_t o = adjacent ? t : order[t];
+        const bool remap = b2 || !adjacent;
+        for (int64_t t = 0; t < nc + (b2 ? 1 : 0); t++) {
+            const int64_t o = remap ? order[t] : t;
+            if (o < 0) {  // B2 pad record
+                uint32_t* rec = static_cast<uint32_t*>(h_nodes) + 2 * (base + t);
+                rec[0] = rec[1] = 0u;
+                continue;
+            }
             const bool leaf = st[o] == 1;
-            const int64_t l = leaf ? 0 : (adjacent ? lf[o] : newid[lf[o]]);
+            const int64_t l = leaf ? 0 : (remap ? newid[lf[o]] : lf[o]);
             if (!leaf && (l < 1 || l >= max_left)) {
                 errs[b] = "tree " + std::to_string(b) + ": child id out of range for layout";
                 return;
@@ -148,7 +202,7 @@ extern "C" int rfxc_forest_pack_host(const void* const* status, const void* cons
                 return;
             }
             const bool cat = !leaf && col_cat[f] == 1;
-            if (layout == RFXC_NODES_F32) {
+            if (layout != RFXC_NODES_F64) {
                 uint32_t x, y;
                 if (leaf) {
                     x = (uint32_t)code[o];
@@ -160,7 +214,13 @@ extern "C" int rfxc_forest_pack_host(const void* const* status, const void* cons
                         float fr = round_down_f32(th[o]);
                         std::memcpy(&x, &fr, 4);
                     }
-                    y = ((uint32_t)l << (fb + 1)) | ((uint32_t)cat << fb) | (uint32_t)f;
+                    if (b2) {  // bit fb+1: the left child is internal
+                        const uint32_t lint = st[lf[o]] == 0 ? 1u : 0u;
+                        y = ((uint32_t)l << (fb + 2)) | (lint << (fb + 1)) | ((uint32_t)cat << fb) |
+                            (uint32_t)f;
+                    } else {
+                        y = ((uint32_t)l << (fb + 1)) | ((uint32_t)cat << fb) | (uint32_t)f;
+                    }
                 }
                 uint32_t* rec = static_cast<uint32_t*>(h_nodes) + 2 * (base + t);
                 rec[0] = x;

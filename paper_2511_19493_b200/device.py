@@ -207,11 +207,22 @@ class DeviceForest:
         self.node_counts = counts
         self.total_nodes = int(counts.sum())
         self.f32_ok = int(counts.max()) < (1 << (31 - feature_bits(self.p)))
+        b2_ok = int(counts.max()) + 1 < (1 << (30 - feature_bits(self.p)))
         if layout is None:
-            layout = _lib.NODES_F32 if self.f32_ok else _lib.NODES_F64
-        if layout == _lib.NODES_F32 and not self.f32_ok:
+            # f32 records in two-level blocks (one dependent load per two
+            # levels); RFX_TRAV_LAYOUT=f32 keeps the reference node order
+            if b2_ok and os.environ.get("RFX_TRAV_LAYOUT", "b2") != "f32":
+                layout = _lib.NODES_F32_B2
+            else:
+                layout = _lib.NODES_F32 if self.f32_ok else _lib.NODES_F64
+        if (layout == _lib.NODES_F32 and not self.f32_ok) or (layout == _lib.NODES_F32_B2 and not b2_ok):
             raise DataError("tree too large for the 8-byte node layout")
+        if layout not in (_lib.NODES_F32, _lib.NODES_F64, _lib.NODES_F32_B2):
+            raise DataError(f"unknown node layout {layout}")
         self.layout = layout
+        rec = 16 if layout == _lib.NODES_F64 else 8
+        # B2: a pad record per tree, 4 spare records after the last one
+        nrec = self.total_nodes + (B + 4 if layout == _lib.NODES_F32_B2 else 0)
         # no categorical column: the traversal skips the per-node category test
         self.numeric = not bool(np.any(col_cat))
 
@@ -226,8 +237,7 @@ class DeviceForest:
                     a = _as(getattr(t, name), dt)
                     keep.append(a)
                     tables[name][b] = a.ctypes.data
-            rec = 8 if layout == _lib.NODES_F32 else 16
-            buf, view = _pinned(self.total_nodes * rec)
+            buf, view = _pinned(nrec * rec)
             off = np.empty(B + 1, dtype=np.int64)
             lc = np.empty(B, dtype=np.int32)
             P = _lib.P
@@ -245,10 +255,9 @@ class DeviceForest:
         self.leaf_counts = lc.copy()
         self.node_off_host = off
         self.node_off = torch.from_numpy(off).to(dev)
-        rec = 8 if layout == _lib.NODES_F32 else 16
         self._rec = rec
         self._staging = buf
-        self._nodes = torch.empty(max(self.total_nodes * rec, 1), dtype=torch.uint8, device=dev)
+        self._nodes = torch.empty(max(nrec * rec, 1), dtype=torch.uint8, device=dev)
         # node records cross PCIe in tree chunks on a copy stream, so the
         # traversal of chunk c overlaps the copy of chunk c + 1 (traverse());
         # a small first chunk lets the traversal start early
@@ -458,17 +467,22 @@ def traverse(dforest: DeviceForest, dvalues: DeviceValues):
     """K1: codes of every sample in every local tree (tm and nb layouts)."""
     torch = _torch()
     layout = dforest.layout
-    if layout == _lib.NODES_F32 and not dvalues.exact_f32:
+    f32 = layout != _lib.NODES_F64
+    if f32 and not dvalues.exact_f32:
         raise DataError("f32 node layout needs f32-exact values")
-    vals = dvalues.f32 if layout == _lib.NODES_F32 else dvalues.f64
+    vals = dvalues.f32 if f32 else dvalues.f64
     n, Bl = dvalues.n, dforest.ntree
     dev = vals.device
     tm = torch.empty((Bl, n), dtype=torch.int32, device=dev)
     cur = torch.cuda.current_stream()
-    f32_rows = dvalues.rows_ready if layout == _lib.NODES_F32 else []
+    f32_rows = dvalues.rows_ready if f32 else []
     done = []  # (c0, c1, event after the chunk's codes)
 
-    klayout = _lib.NODES_F32_NUMERIC if layout == _lib.NODES_F32 and dforest.numeric else layout
+    klayout = layout
+    if dforest.numeric and layout == _lib.NODES_F32:
+        klayout = _lib.NODES_F32_NUMERIC
+    elif dforest.numeric and layout == _lib.NODES_F32_B2:
+        klayout = _lib.NODES_F32_B2_NUMERIC
 
     def walk(c0, c1, lo, hi):
         _lib.call("rfxc_leaf_codes_rows", _lib.ptr(dforest._nodes), _lib.ptr(dforest.node_off),

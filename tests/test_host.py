@@ -84,8 +84,9 @@ def host_pack(trees, p, col_cat, layout):
         keep += arrs
         tabs.append(np.array([a.ctypes.data for a in arrs], dtype=np.uintp))
     counts = np.array([len(t.status) for t in trees], dtype=np.int64)
-    rec = 8 if layout == _lib.NODES_F32 else 16
-    out = np.zeros(int(counts.sum()) * rec, dtype=np.uint8)
+    rec = 16 if layout == _lib.NODES_F64 else 8
+    extra = B + 4 if layout == _lib.NODES_F32_B2 else 0  # pad record per tree + 4 spare
+    out = np.zeros((int(counts.sum()) + extra) * rec, dtype=np.uint8)
     off = np.empty(B + 1, np.int64)
     lc = np.empty(B, np.int32)
     cc = np.ascontiguousarray(col_cat, dtype=np.uint8)
@@ -113,6 +114,70 @@ def walk_f32(rec, off, b, x, p):
         else:
             go = v <= np.uint32(w0).view(np.float32)
         node = left + (0 if go else 1)
+
+
+def walk_b2(rec, off, b, x, p):
+    """Decode the two-level block layout and descend two levels per block
+    fetch (mirror of traverse_kernel's B2 path)."""
+    from paper_2511_19493_b200.device import feature_bits
+    fb = feature_bits(p)
+    words = rec.view(np.uint32).reshape(-1, 2)
+    o = int(off[b])
+
+    def decide(w0, w1):
+        f, cat = w1 & ((1 << fb) - 1), (w1 >> fb) & 1
+        v = np.float32(x[f])
+        if cat:
+            return ((w0 >> int(v)) & 1) == 1 if int(v) < 32 else False
+        return v <= np.uint32(w0).view(np.float32)
+
+    w0, w1 = int(words[o, 0]), int(words[o, 1])
+    while True:
+        if w1 == 0:
+            return w0
+        go = decide(w0, w1)
+        blk, lint = w1 >> (fb + 2), (w1 >> (fb + 1)) & 1
+        assert blk % 2 == 0  # children pairs are 16-byte aligned
+        y0, y1 = int(words[o + blk + (0 if go else 1), 0]), int(words[o + blk + (0 if go else 1), 1])
+        pair = o + blk + 2 + (2 if (not go and lint) else 0)
+        if y1 == 0:
+            return y0
+        assert (y1 >> (fb + 2)) == pair - o  # the child's children pair is where the kernel looks
+        g = pair if decide(y0, y1) else pair + 1
+        w0, w1 = int(words[g, 0]), int(words[g, 1])
+
+
+def test_host_packer_b2_layout(orc, mixed):
+    """Two-level block layout: same leaf codes as the reference on a trained
+    mixed (categorical) forest and on the hand-built tree with right != left+1,
+    one pad record per tree, pairs 16-byte aligned."""
+    from conftest import golden
+    from paper_2511_19493_b200 import _lib
+    ds, forest = mixed
+    X = ds.values.astype(np.float32).astype(np.float64)
+    codes, lc_ref = orc.leaf_membership(forest.trees, forest.col_cat, X)
+    rec, off, lc = host_pack(forest.trees, ds.p, forest.col_cat, _lib.NODES_F32_B2)
+    assert np.array_equal(lc, lc_ref)
+    assert np.array_equal(np.diff(off), [len(t.status) + 1 for t in forest.trees])
+    assert np.all(off % 2 == 0)
+    for i in range(0, ds.n, 5):
+        for b in range(0, forest.ntree, 2):
+            assert walk_b2(rec, off, b, X[i], ds.p) == codes[i, b]
+
+    class T:
+        pass
+    h = golden("handbuilt.npz")
+    t = T()
+    t.status, t.split_var, t.threshold = h["status"], h["split_var"], h["threshold"]
+    t.cat_mask, t.left, t.right = np.zeros(7, np.int64), h["left"], h["right"]
+    stump = T()  # a single-leaf tree
+    stump.status, stump.split_var, stump.threshold = np.array([1], np.int8), np.zeros(1), np.zeros(1)
+    stump.cat_mask, stump.left, stump.right = np.zeros(1, np.int64), np.zeros(1), np.zeros(1)
+    rec, off, lc = host_pack([t, stump], 2, np.zeros(2), _lib.NODES_F32_B2)
+    assert list(lc) == [4, 1]
+    for x, want in zip(h["points"], h["codes"]):
+        assert walk_b2(rec, off, 0, x, 2) == want
+        assert walk_b2(rec, off, 1, x, 2) == 0
 
 
 def test_host_packer_relayout_keeps_codes(built):
