@@ -44,15 +44,15 @@ enum { RFXC_NODES_F32 = 0, /* 8 B/node, thresholds rounded down to f32 */
        RFXC_NODES_F64 = 1, /* 16 B/node, f64 thresholds             */
        RFXC_NODES_F32_NUMERIC = 2, /* traversal only: F32 records of a forest with
                                       no categorical column (no category test per node) */
-       RFXC_NODES_F32_B2 = 3, /* F32 records in two-level blocks (host packer only):
-                                 per tree [root, pad, blocks...], block(x) for every
-                                 internal node x at even depth = x's children pair,
-                                 then the children pairs of those children that are
-                                 internal; a record's left id points at its children
-                                 pair, bit fb+1 says whether the left child is
-                                 internal.  Tree b holds node_counts[b] + 1 records;
-                                 the buffer needs 4 spare records after the last tree.
-                                 The traversal takes two levels per dependent load. */
+       RFXC_NODES_F32_B2 = 3, /* F32 records in 32-byte two-level groups (host packer
+                                 only): per tree [root, pad x3], then for every internal
+                                 node x at even depth group0 = [L, R, L's children pair]
+                                 and, if R is internal, group1 = [R (copy), pad, R's
+                                 children pair]; x's record points at group0, bit fb+1
+                                 = "R internal".  One 256-bit load per two levels.  The
+                                 record count per tree depends on the shape: call
+                                 rfxc_forest_pack_host with h_nodes = NULL first (fills
+                                 h_node_off / h_leaf_counts only). */
        RFXC_NODES_F32_B2_NUMERIC = 4 /* traversal only: B2 records, no categorical column */ };
 
 /* Output layouts of rfxc_pair_counts. */

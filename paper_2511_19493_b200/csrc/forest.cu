@@ -214,39 +214,43 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
                 if (!(actm & (1u << c))) continue;
                 if (B2) {
                     // two levels per dependent load: decide at block root x,
-                    // then fetch the chosen child's record and (in the same
-                    // round trip) its children pair, decide at the child
+                    // then one 256-bit load brings the chosen child's record
+                    // and that child's children pair; decide at the child
                     const uint2 nd = xr[c];
                     if (nd.y == 0u) {
                         code[c] = (int32_t)nd.x;
                         actm &= ~(1u << c);
                         continue;
                     }
-                    auto decide = [&](const uint2 r) {
-                        const uint32_t f = r.y & fmask;
+                    auto decide = [&](const uint32_t rx, const uint32_t ry) {
+                        const uint32_t f = ry & fmask;
                         float v;
                         if (SMEM_X)
                             asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(xaddr + 4u * f));
                         else
                             v = (float)X[(int64_t)f * n + i];
-                        if (!NUMERIC && ((r.y >> fb) & 1u)) {
+                        if (!NUMERIC && ((ry >> fb) & 1u)) {
                             const uint32_t lv = (uint32_t)(int)v;
-                            return lv < 32u ? (bool)((r.x >> lv) & 1u) : false;
+                            return lv < 32u ? (bool)((rx >> lv) & 1u) : false;
                         }
-                        return v <= __uint_as_float(r.x);
+                        return v <= __uint_as_float(rx);
                     };
-                    const bool go = decide(nd);
-                    const uint32_t blk = nd.y >> (fb + 2);
-                    const uint32_t lint = (nd.y >> (fb + 1)) & 1u;
-                    const uint2 yr = __ldg(nptr[c] + blk + (go ? 0u : 1u));
-                    const uint4 pr =
-                        __ldg(reinterpret_cast<const uint4*>(nptr[c] + blk + 2u + ((!go && lint) ? 2u : 0u)));
-                    if (yr.y == 0u) {
-                        code[c] = (int32_t)yr.x;
+                    const bool go = decide(nd.x, nd.y);
+                    const bool rint = (nd.y >> (fb + 1)) & 1u;
+                    const uint32_t g = (nd.y >> (fb + 2)) + ((!go && rint) ? 4u : 0u);
+                    uint32_t a[8];
+                    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                 : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]),
+                                   "=r"(a[6]), "=r"(a[7])
+                                 : "l"(nptr[c] + g));
+                    const bool first = go || rint;  // group1 starts with R's copy
+                    const uint32_t yx = first ? a[0] : a[2], yy = first ? a[1] : a[3];
+                    if (yy == 0u) {
+                        code[c] = (int32_t)yx;
                         actm &= ~(1u << c);
                         continue;
                     }
-                    xr[c] = decide(yr) ? make_uint2(pr.x, pr.y) : make_uint2(pr.z, pr.w);
+                    xr[c] = decide(yx, yy) ? make_uint2(a[4], a[5]) : make_uint2(a[6], a[7]);
                 } else if (LAYOUT == RFXC_NODES_F32) {
                     const uint2 nd = (TOP > 0 && id[c] < (uint32_t)TOP)
                                          ? tops[(grp * TRAV_ILP + c) * TOP + id[c]]

@@ -221,8 +221,6 @@ class DeviceForest:
             raise DataError(f"unknown node layout {layout}")
         self.layout = layout
         rec = 16 if layout == _lib.NODES_F64 else 8
-        # B2: a pad record per tree, 4 spare records after the last one
-        nrec = self.total_nodes + (B + 4 if layout == _lib.NODES_F32_B2 else 0)
         # no categorical column: the traversal skips the per-node category test
         self.numeric = not bool(np.any(col_cat))
 
@@ -237,17 +235,24 @@ class DeviceForest:
                     a = _as(getattr(t, name), dt)
                     keep.append(a)
                     tables[name][b] = a.ctypes.data
-            buf, view = _pinned(nrec * rec)
             off = np.empty(B + 1, dtype=np.int64)
             lc = np.empty(B, dtype=np.int32)
             P = _lib.P
-            with region("forest_pack_host"):
+
+            def pack(dst):
                 _lib.call("rfxc_forest_pack_host", *(tables[k].ctypes.data_as(P) for k in
                                                      ("status", "split_var", "threshold",
                                                       "cat_mask", "left", "right")),
                           counts.ctypes.data_as(P), B, col_cat.ctypes.data_as(P), self.p, layout,
-                          view.ctypes.data_as(P), off.ctypes.data_as(P), lc.ctypes.data_as(P),
-                          nthreads)
+                          dst, off.ctypes.data_as(P), lc.ctypes.data_as(P), nthreads)
+
+            with region("forest_pack_host"):
+                nrec = self.total_nodes
+                if layout == _lib.NODES_F32_B2:  # sizing call: the record count per tree
+                    pack(None)
+                    nrec = int(off[B])
+                buf, view = _pinned(nrec * rec)
+                pack(view.ctypes.data_as(P))
             del keep
             return buf, off, lc
 
@@ -257,7 +262,7 @@ class DeviceForest:
         self.node_off = torch.from_numpy(off).to(dev)
         self._rec = rec
         self._staging = buf
-        self._nodes = torch.empty(max(nrec * rec, 1), dtype=torch.uint8, device=dev)
+        self._nodes = torch.empty(max(int(off[B]) * rec, 1), dtype=torch.uint8, device=dev)
         # node records cross PCIe in tree chunks on a copy stream, so the
         # traversal of chunk c overlaps the copy of chunk c + 1 (traverse());
         # a small first chunk lets the traversal start early

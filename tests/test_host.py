@@ -85,15 +85,21 @@ def host_pack(trees, p, col_cat, layout):
         tabs.append(np.array([a.ctypes.data for a in arrs], dtype=np.uintp))
     counts = np.array([len(t.status) for t in trees], dtype=np.int64)
     rec = 16 if layout == _lib.NODES_F64 else 8
-    extra = B + 4 if layout == _lib.NODES_F32_B2 else 0  # pad record per tree + 4 spare
-    out = np.zeros((int(counts.sum()) + extra) * rec, dtype=np.uint8)
     off = np.empty(B + 1, np.int64)
     lc = np.empty(B, np.int32)
     cc = np.ascontiguousarray(col_cat, dtype=np.uint8)
     P = ctypes.c_void_p
-    _lib.call("rfxc_forest_pack_host", *(t.ctypes.data_as(P) for t in tabs),
-              counts.ctypes.data_as(P), B, cc.ctypes.data_as(P), p, layout,
-              out.ctypes.data_as(P), off.ctypes.data_as(P), lc.ctypes.data_as(P), 2)
+
+    def call(dst):
+        _lib.call("rfxc_forest_pack_host", *(t.ctypes.data_as(P) for t in tabs),
+                  counts.ctypes.data_as(P), B, cc.ctypes.data_as(P), p, layout,
+                  dst, off.ctypes.data_as(P), lc.ctypes.data_as(P), 2)
+    nrec = int(counts.sum())
+    if layout == _lib.NODES_F32_B2:  # sizing call first
+        call(None)
+        nrec = int(off[B])
+    out = np.zeros(nrec * rec, dtype=np.uint8)
+    call(out.ctypes.data_as(P))
     return out, off, lc
 
 
@@ -117,7 +123,7 @@ def walk_f32(rec, off, b, x, p):
 
 
 def walk_b2(rec, off, b, x, p):
-    """Decode the two-level block layout and descend two levels per block
+    """Decode the 32-byte two-level groups and descend two levels per group
     fetch (mirror of traverse_kernel's B2 path)."""
     from paper_2511_19493_b200.device import feature_bits
     fb = feature_bits(p)
@@ -136,21 +142,21 @@ def walk_b2(rec, off, b, x, p):
         if w1 == 0:
             return w0
         go = decide(w0, w1)
-        blk, lint = w1 >> (fb + 2), (w1 >> (fb + 1)) & 1
-        assert blk % 2 == 0  # children pairs are 16-byte aligned
-        y0, y1 = int(words[o + blk + (0 if go else 1), 0]), int(words[o + blk + (0 if go else 1), 1])
-        pair = o + blk + 2 + (2 if (not go and lint) else 0)
-        if y1 == 0:
-            return y0
-        assert (y1 >> (fb + 2)) == pair - o  # the child's children pair is where the kernel looks
-        g = pair if decide(y0, y1) else pair + 1
-        w0, w1 = int(words[g, 0]), int(words[g, 1])
+        rint = (w1 >> (fb + 1)) & 1
+        g = o + (w1 >> (fb + 2)) + (4 if (not go and rint) else 0)
+        assert (g - o) % 4 == 0  # 32-byte groups
+        a = words[g:g + 4]
+        y = a[0] if (go or rint) else a[1]
+        if int(y[1]) == 0:
+            return int(y[0])
+        n2 = a[2] if decide(int(y[0]), int(y[1])) else a[3]
+        w0, w1 = int(n2[0]), int(n2[1])
 
 
 def test_host_packer_b2_layout(orc, mixed):
-    """Two-level block layout: same leaf codes as the reference on a trained
-    mixed (categorical) forest and on the hand-built tree with right != left+1,
-    one pad record per tree, pairs 16-byte aligned."""
+    """Two-level group layout: same leaf codes as the reference on a trained
+    mixed (categorical) forest and on the hand-built tree with right != left+1
+    (plus a single-leaf tree); trees and groups 32-byte aligned."""
     from conftest import golden
     from paper_2511_19493_b200 import _lib
     ds, forest = mixed
@@ -158,8 +164,7 @@ def test_host_packer_b2_layout(orc, mixed):
     codes, lc_ref = orc.leaf_membership(forest.trees, forest.col_cat, X)
     rec, off, lc = host_pack(forest.trees, ds.p, forest.col_cat, _lib.NODES_F32_B2)
     assert np.array_equal(lc, lc_ref)
-    assert np.array_equal(np.diff(off), [len(t.status) + 1 for t in forest.trees])
-    assert np.all(off % 2 == 0)
+    assert np.all(off % 4 == 0) and np.all(np.diff(off) >= [len(t.status) for t in forest.trees])
     for i in range(0, ds.n, 5):
         for b in range(0, forest.ntree, 2):
             assert walk_b2(rec, off, b, X[i], ds.p) == codes[i, b]
