@@ -35,12 +35,22 @@ sha = hashlib.sha256(tm.cpu().numpy().tobytes()).hexdigest()[:16]
 print(f"traverse {ev[0].elapsed_time(ev[1]) / 5:.3f} ms  (n={N}, p={P}, trees={B}) codes {sha}",
       flush=True)
 
-if len(sys.argv) > 5 and sys.argv[5] == "sorted":
+if len(sys.argv) > 5 and sys.argv[5] in ("sorted", "strided"):
     # the same traversal with the samples reordered by their leaf in tree 0
     # (neighbouring lanes then share most of their paths)
     import numpy as np
     from paper_2511_19493_b200.dataset import from_arrays as fa
     order = np.argsort(tm[0].cpu().numpy(), kind="stable")
+    if sys.argv[5] == "strided":
+        # 128-sample tiles stay coherent, but consecutive tiles (the CTAs
+        # resident together) come from far-apart parts of the sorted order
+        tiles = (N + 127) // 128
+        stride = max(1, tiles // 296) | 1
+        while np.gcd(stride, tiles) != 1:
+            stride += 2
+        pt = (np.arange(tiles) * stride) % tiles
+        parts = [order[t * 128:(t + 1) * 128] for t in pt]
+        order = np.concatenate(parts)
     ds2 = fa(np.ascontiguousarray(X[order]), y[order])
     dv2 = DeviceValues(ds2.values)
     for _ in range(3):
@@ -52,5 +62,5 @@ if len(sys.argv) > 5 and sys.argv[5] == "sorted":
     ev[1].record()
     torch.cuda.synchronize()
     same = bool((tm2.cpu().numpy() == tm.cpu().numpy()[:, order]).all())
-    print(f"sorted by tree-0 leaf: traverse {ev[0].elapsed_time(ev[1]) / 5:.3f} ms, codes permuted "
+    print(f"{sys.argv[5]} by tree-0 leaf: traverse {ev[0].elapsed_time(ev[1]) / 5:.3f} ms, codes permuted "
           f"equal: {same}", flush=True)
