@@ -185,6 +185,66 @@ def test_host_packer_b2_layout(orc, mixed):
         assert walk_b2(rec, off, 1, x, 2) == 0
 
 
+def _random_tree(rng, n_internal, p, caterpillar=False):
+    """Breadth-first numbered binary tree (siblings adjacent) of random shape;
+    caterpillar=True: every right child is a leaf (depth = n_internal)."""
+    class T:
+        pass
+    status, left = [0], [0]
+    frontier = [0]
+    made = 1
+    while made < n_internal:
+        x = frontier.pop(rng.integers(len(frontier)) if not caterpillar else 0)
+        left[x] = len(status)
+        for c in range(2):
+            status.append(1)
+            left.append(0)
+        for c, ch in enumerate((left[x], left[x] + 1)):
+            if made < n_internal and (c == 0 if caterpillar else rng.random() < 0.9):
+                status[ch] = 0
+                frontier.append(ch)
+                made += 1
+        if not frontier:
+            break
+    for x in frontier:  # unexpanded internal nodes become leaves
+        status[x] = 1
+    # renumber breadth-first (siblings adjacent) from the root
+    nodes, q = [0], 0
+    while q < len(nodes):
+        x = nodes[q]
+        q += 1
+        if status[x] == 0:
+            nodes += [left[x], left[x] + 1]
+    new = {o: i for i, o in enumerate(nodes)}
+    t = T()
+    m = len(nodes)
+    t.status = np.array([status[o] for o in nodes], np.int8)
+    t.left = np.array([new[left[o]] if status[o] == 0 else 0 for o in nodes], np.int32)
+    t.right = np.where(t.status == 0, t.left + 1, 0).astype(np.int32)
+    t.split_var = rng.integers(0, p, m).astype(np.int32)
+    t.threshold = rng.normal(size=m)
+    t.cat_mask = np.zeros(m, np.int64)
+    return t
+
+
+@pytest.mark.parametrize("shape", ["random", "caterpillar"])
+def test_host_packer_b2_random_shapes(built, shape):
+    """Random and maximally unbalanced trees: the two-level groups route every
+    point like the reference node order."""
+    from paper_2511_19493_b200 import _lib
+    rng = np.random.default_rng(11 if shape == "random" else 12)
+    p = 5
+    trees = [_random_tree(rng, int(k), p, caterpillar=(shape == "caterpillar"))
+             for k in rng.integers(1, 300, size=6)]
+    r1, o1, l1 = host_pack(trees, p, np.zeros(p), _lib.NODES_F32)
+    r2, o2, l2 = host_pack(trees, p, np.zeros(p), _lib.NODES_F32_B2)
+    assert np.array_equal(l1, l2)
+    pts = rng.normal(size=(200, p)).astype(np.float32).astype(np.float64)
+    for b in range(len(trees)):
+        for x in pts:
+            assert walk_b2(r2, o2, b, x, p) == walk_f32(r1, o1, b, x, p)
+
+
 def test_host_packer_relayout_keeps_codes(built):
     """Hand-built tree with right != left + 1 (tests/test_forest.py:170-185):
     relaid out breadth-first by the C++ packer, leaf ordinals preserved."""
