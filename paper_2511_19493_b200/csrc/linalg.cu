@@ -181,13 +181,16 @@ __global__ void __launch_bounds__(LA_THREADS) eig_map_kernel(const double* __res
     }
 }
 
+#ifndef RFXC_CHOL_THREADS
+#define RFXC_CHOL_THREADS 512
+#endif
 // Rinv (k x k, upper) with G + shift_rel tr(G) I = R^T R (Cholesky of the
 // symmetrised matrix); a non-positive pivot gives a zero row/column.  One CTA,
 // one barrier per step: step j updates the trailing upper triangle with the
 // unscaled row j (a_ab -= a_ja a_jb / a_jj, every thread reads the pivot
 // itself), rows are scaled at the end; the inverse is column-oriented back
 // substitution (step m finalises row m of R^-1 and updates every row above).
-constexpr int CHOL_THREADS = 256;
+constexpr int CHOL_THREADS = RFXC_CHOL_THREADS;
 
 __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const double* __restrict__ Gin,
                                                                 int k, double shift_rel,
@@ -211,15 +214,16 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const double* __
     if (shift_rel > 0.0)
         for (int i = tid; i < k; i += nt) R[i * k + i] += shift_rel * tr;
     __syncthreads();
-    // step j: trailing upper triangle a_ab -= a_ja a_jb / a_jj (unscaled row j)
+    // step j: trailing upper triangle a_ab -= a_ja a_jb / a_jj (unscaled row
+    // j); rows over warps, columns over lanes (no index division)
+    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     for (int j = 0; j < k - 1; j++) {
         const double d = R[j * k + j];
-        const int m = k - j - 1;
         if (d > 0.0) {
             const double inv = 1.0 / d;
-            for (int e = tid; e < m * m; e += nt) {
-                const int a = j + 1 + e / m, b = j + 1 + e % m;
-                if (b >= a) R[a * k + b] -= R[j * k + a] * R[j * k + b] * inv;
+            for (int a = j + 1 + warp; a < k; a += nw) {
+                const double rja = R[j * k + a];
+                for (int b = a + lane; b < k; b += 32) R[a * k + b] -= rja * R[j * k + b] * inv;
             }
         }
         __syncthreads();
@@ -242,9 +246,9 @@ __global__ void __launch_bounds__(CHOL_THREADS) chol_inv_kernel(const double* __
             X[m * k + m + c] = rmm > 0.0 ? v / rmm : 0.0;
         }
         __syncthreads();
-        for (int e = tid; e < m * w; e += nt) {
-            const int i = e / w, c = m + e % w;
-            X[i * k + c] -= R[i * k + m] * X[m * k + c];
+        for (int i = warp; i < m; i += nw) {
+            const double rim = R[i * k + m];
+            for (int c = m + lane; c < k; c += 32) X[i * k + c] -= rim * X[m * k + c];
         }
         __syncthreads();
     }
