@@ -140,6 +140,23 @@ int rfxc_h2d_rows(void* d_dst, const void* h_src, int64_t n, int64_t p, int32_t 
 /* (rows, cols) int32 transpose: tm <-> nb layouts. */
 int rfxc_transpose_i32(const int32_t* d_in, int64_t rows, int64_t cols,
                        int32_t* d_out, void* stream);
+/* General form: d_out[map(c) * ld_out + r] = d_in[r * ld_in + c] for r < rows,
+ * c < cols (map = identity when d_col_map is NULL).  The traversal uses it to
+ * bring the codes of samples walked in leaf order back to sample order. */
+int rfxc_transpose_i32_ex(const int32_t* d_in, int64_t rows, int64_t cols, int64_t ld_in,
+                          int32_t* d_out, int64_t ld_out, const int32_t* d_col_map,
+                          void* stream);
+
+/* K1 helpers (no reference counterpart; traversal scheduling only): d_order (n)
+ * = the samples grouped by their leaf code in d_codes (one tree, codes <
+ * nleaf; d_scratch: nleaf ints), so a traversal tile's samples share paths;
+ * the order inside a leaf is not reproducible and never changes a code.
+ * rfxc_permute_rows_f32: d_Xp[f * n + j] = d_X[f * n + d_order[j]]
+ * (column-major (n, p) values in that order). */
+int rfxc_leaf_order(const int32_t* d_codes, int64_t n, int32_t nleaf, int32_t* d_order,
+                    int32_t* d_scratch, void* stream);
+int rfxc_permute_rows_f32(const float* d_X, int64_t n, int32_t p, const int32_t* d_order,
+                          float* d_Xp, void* stream);
 
 /* OOB votes (oob_votes_tree, _kernels.py:377-385; forest.py:287-290) from
  * the leaf codes: d_votes (n, C) int64 = #{trees b with d_inbag[b, i] == 0

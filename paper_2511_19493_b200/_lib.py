@@ -40,6 +40,9 @@ SIGNATURES = {
     "rfxc_values_to_f32_host": (ctypes.c_int, [P, I64, P, P, I32]),
     "rfxc_leaf_codes": (ctypes.c_int, [P, P, I32, I32, I32, I32, P, I64, P, P]),
     "rfxc_transpose_i32": (ctypes.c_int, [P, I64, I64, P, P]),
+    "rfxc_transpose_i32_ex": (ctypes.c_int, [P, I64, I64, I64, P, I64, P, P]),
+    "rfxc_leaf_order": (ctypes.c_int, [P, I64, I32, P, P, P]),
+    "rfxc_permute_rows_f32": (ctypes.c_int, [P, I64, I32, P, P, P]),
     "rfxc_bucket_scratch_bytes": (I64, [I64, I32]),
     "rfxc_outlier_work_bytes": (I64, [I64]),
     "rfxc_leaf_codes_rows": (ctypes.c_int, [P, P, I32, I32, I32, I32, P, I64, I64, I64, P, P]),
@@ -121,7 +124,8 @@ def check(rc: int, what: str = "") -> None:
 # kernels launched per successful call (host-side count for bench.py's
 # gpu_launches; rfxc_gram / rfxc_mds_power add their data-dependent extras)
 LAUNCHES = {"rfxc_values_to_f32": 1, "rfxc_forest_pack": 1, "rfxc_leaf_codes": 1,
-            "rfxc_transpose_i32": 1, "rfxc_bucket": 1, "rfxc_bucket_trees": 1, "rfxc_pair_counts": 1,
+            "rfxc_transpose_i32": 1, "rfxc_transpose_i32_ex": 1, "rfxc_leaf_order": 3,
+            "rfxc_permute_rows_f32": 1, "rfxc_bucket": 1, "rfxc_bucket_trees": 1, "rfxc_pair_counts": 1,
             "rfxc_triblock_count": 1, "rfxc_triblock_emit": 1, "rfxc_exclusive_scan_i64": 1,
             "rfxc_normals": 1, "rfxc_pack_f32": 1, "rfxc_leaf_sums": 1, "rfxc_leaf_gather": 1,
             "rfxc_sketch_prepare": 1, "rfxc_sketch_pass": 1, "rfxc_orth_map": 1,

@@ -301,19 +301,80 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
     }
 }
 
+// out[map(c) * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols
+// (map = identity when col_map is null): 32 x 32 tiles through shared memory
 __global__ void transpose_i32_kernel(const int32_t* __restrict__ in, int64_t rows,
-                                     int64_t cols, int32_t* __restrict__ out)
+                                     int64_t cols, int64_t ld_in, int32_t* __restrict__ out,
+                                     int64_t ld_out, const int32_t* __restrict__ col_map)
 {
     __shared__ int32_t tile[32][33];
     const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
         int64_t r = r0 + k, c = c0 + threadIdx.x;
-        if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * cols + c];
+        if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * ld_in + c];
     }
     __syncthreads();
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
         int64_t c = c0 + k, r = r0 + threadIdx.x;
-        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+        if (r < rows && c < cols) {
+            const int64_t oc = col_map ? (int64_t)__ldg(col_map + c) : c;
+            out[oc * ld_out + r] = tile[threadIdx.x][k];
+        }
+    }
+}
+
+// Sample order for the traversal: samples grouped by their leaf in one tree
+// (counts, exclusive scan, scatter).  The slot of a sample inside its leaf's
+// group comes from an atomic and is not reproducible — only which samples
+// share a traversal tile depends on it, never a leaf code.
+__global__ void leaf_hist_kernel(const int32_t* __restrict__ codes, int64_t n, int32_t* __restrict__ cnt)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(cnt + __ldg(codes + i), 1);
+}
+
+__global__ void __launch_bounds__(1024) leaf_scan_kernel(int32_t* __restrict__ cnt, int nleaf)
+{
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t carry;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nleaf; base += 1024) {
+        const int i = base + (int)threadIdx.x;
+        const int v = i < nleaf ? cnt[i] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        int before = carry;
+        for (int w = 0; w < warp; w++) before += wsum[w];
+        if (i < nleaf) cnt[i] = before + x - v;  // exclusive
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = before + x;
+        __syncthreads();
+    }
+}
+
+__global__ void leaf_scatter_kernel(const int32_t* __restrict__ codes, int64_t n, int32_t* __restrict__ cur,
+                                    int32_t* __restrict__ order)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        order[atomicAdd(cur + __ldg(codes + i), 1)] = (int32_t)i;
+}
+
+// Xp[f * n + j] = X[f * n + order[j]] (column-major (n, p) f32 values)
+__global__ void permute_rows_f32_kernel(const float* __restrict__ X, int64_t n, int p,
+                                        const int32_t* __restrict__ order, float* __restrict__ Xp)
+{
+    const int64_t total = n * p;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = q / n, j = q - f * n;
+        Xp[q] = __ldg(X + f * n + __ldg(order + j));
     }
 }
 
@@ -475,14 +536,46 @@ extern "C" int rfxc_h2d_rows(void* d_dst, const void* h_src, int64_t n, int64_t 
     return RFXC_OK;
 }
 
+extern "C" int rfxc_transpose_i32_ex(const int32_t* d_in, int64_t rows, int64_t cols, int64_t ld_in,
+                                     int32_t* d_out, int64_t ld_out, const int32_t* d_col_map,
+                                     void* stream)
+{
+    if (rows < 0 || cols < 0 || ld_in < cols || ld_out < rows)
+        return fail(RFXC_EDATA, "transpose: bad shape");
+    if (rows == 0 || cols == 0) return RFXC_OK;
+    dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+    transpose_i32_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(d_in, rows, cols, ld_in, d_out, ld_out,
+                                                                       d_col_map);
+    return check_launch("transpose_i32");
+}
+
 extern "C" int rfxc_transpose_i32(const int32_t* d_in, int64_t rows, int64_t cols,
                                   int32_t* d_out, void* stream)
 {
-    if (rows < 0 || cols < 0) return fail(RFXC_EDATA, "transpose: bad shape");
-    if (rows == 0 || cols == 0) return RFXC_OK;
-    dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
-    transpose_i32_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(d_in, rows, cols, d_out);
-    return check_launch("transpose_i32");
+    return rfxc_transpose_i32_ex(d_in, rows, cols, cols, d_out, rows, nullptr, stream);
+}
+
+extern "C" int rfxc_leaf_order(const int32_t* d_codes, int64_t n, int32_t nleaf, int32_t* d_order,
+                               int32_t* d_scratch, void* stream)
+{
+    if (n < 1 || nleaf < 1) return fail(RFXC_EDATA, "leaf_order: bad shape");
+    cudaStream_t st = as_stream(stream);
+    cudaError_t e = cudaMemsetAsync(d_scratch, 0, (size_t)nleaf * 4, st);
+    if (e != cudaSuccess) return fail(RFXC_ECUDA, "leaf_order: %s", cudaGetErrorString(e));
+    const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 8);
+    leaf_hist_kernel<<<grid, 256, 0, st>>>(d_codes, n, d_scratch);
+    leaf_scan_kernel<<<1, 1024, 0, st>>>(d_scratch, nleaf);
+    leaf_scatter_kernel<<<grid, 256, 0, st>>>(d_codes, n, d_scratch, d_order);
+    return check_launch("leaf_order");
+}
+
+extern "C" int rfxc_permute_rows_f32(const float* d_X, int64_t n, int32_t p, const int32_t* d_order,
+                                     float* d_Xp, void* stream)
+{
+    if (n < 1 || p < 1) return fail(RFXC_EDATA, "permute_rows: bad shape");
+    const int grid = (int)std::min<int64_t>(ceil_div(n * p, 256), (int64_t)sm_count() * 16);
+    permute_rows_f32_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_X, n, p, d_order, d_Xp);
+    return check_launch("permute_rows_f32");
 }
 
 // ------------------------------------------------------------- OOB votes

@@ -64,6 +64,11 @@ def _staged(obj, key, build):
 
 
 UPLOAD_CHUNK_TREES = 128
+# K1 walks the trees after the first chunk in tree-0 leaf order when there
+# are enough samples and trees to repay the order, the permuted values copy
+# and the extra transpose (RFX_TRAV_ORDER=0 keeps sample order)
+TRAV_ORDER_MIN_N = 32768
+TRAV_ORDER_MIN_TREES = 64
 UPLOAD_FIRST_TREES = 32
 _COPY_STREAMS: dict = {}
 
@@ -489,10 +494,10 @@ def traverse(dforest: DeviceForest, dvalues: DeviceValues):
     elif dforest.numeric and layout == _lib.NODES_F32_B2:
         klayout = _lib.NODES_F32_B2_NUMERIC
 
-    def walk(c0, c1, lo, hi):
+    def walk(c0, c1, lo, hi, out=None, values=None):
         _lib.call("rfxc_leaf_codes_rows", _lib.ptr(dforest._nodes), _lib.ptr(dforest.node_off),
-                  klayout, dvalues.p, c0, c1, _lib.ptr(vals), n, lo, hi, _lib.ptr(tm[c0:c1]),
-                  _lib.stream_handle())
+                  klayout, dvalues.p, c0, c1, _lib.ptr(vals if values is None else values), n, lo, hi,
+                  _lib.ptr(tm[c0:c1] if out is None else out), _lib.stream_handle())
 
     def mark(c0, c1):
         cev = torch.cuda.Event()
@@ -517,10 +522,46 @@ def traverse(dforest: DeviceForest, dvalues: DeviceValues):
                         mark(c0, c1)
         if rest and dvalues.ready is not None:
             cur.wait_event(dvalues.ready)
-        for c0, c1, ev in rest:  # after its node records arrived
+        ordered = (f32 and n >= TRAV_ORDER_MIN_N and os.environ.get("RFX_TRAV_ORDER", "1") != "0"
+                   and sum(c1 - c0 for c0, c1, _ in rest) >= TRAV_ORDER_MIN_TREES)
+        if ordered and not done:  # tree 0 first, in sample order
+            (c0, c1, ev), rest = rest[0], rest[1:]
             cur.wait_event(ev)
             walk(c0, c1, 0, n)
             mark(c0, c1)
+            ordered = sum(b - a for a, b, _ in rest) >= TRAV_ORDER_MIN_TREES
+        if not ordered:
+            for c0, c1, ev in rest:  # after its node records arrived
+                cur.wait_event(ev)
+                walk(c0, c1, 0, n)
+                mark(c0, c1)
     nb = torch.empty((n, Bl), dtype=torch.int32, device=dev)
-    _lib.call("rfxc_transpose_i32", _lib.ptr(tm), Bl, n, _lib.ptr(nb), _lib.stream_handle())
+    if not ordered or not rest:
+        _lib.call("rfxc_transpose_i32", _lib.ptr(tm), Bl, n, _lib.ptr(nb), _lib.stream_handle())
+        return nb, tm, done
+    # the remaining trees walk the samples grouped by their tree-0 leaf
+    # (neighbouring lanes share paths: fewer node lines per gather); their
+    # codes come back to sample order through the transpose
+    e = rest[0][0]
+    with region("leaf_codes"):
+        order = torch.empty(n, dtype=torch.int32, device=dev)
+        nl0 = int(dforest.leaf_counts[0])
+        scratch = torch.empty(max(nl0, 1), dtype=torch.int32, device=dev)
+        _lib.call("rfxc_leaf_order", _lib.ptr(tm[0]), n, nl0, _lib.ptr(order), _lib.ptr(scratch),
+                  _lib.stream_handle())
+        xp = torch.empty_like(vals)
+        _lib.call("rfxc_permute_rows_f32", _lib.ptr(vals), n, dvalues.p, _lib.ptr(order), _lib.ptr(xp),
+                  _lib.stream_handle())
+        tp = torch.empty((Bl - e, n), dtype=torch.int32, device=dev)
+        for c0, c1, ev in rest:
+            cur.wait_event(ev)
+            walk(c0, c1, 0, n, out=tp[c0 - e:c1 - e], values=xp)
+        h = _lib.stream_handle()
+        _lib.call("rfxc_transpose_i32_ex", _lib.ptr(tm), e, n, n, _lib.ptr(nb), Bl, None, h)
+        nbe = nb[:, e:]  # column block e.. of the (n, Bl) codes (row stride Bl)
+        _lib.call("rfxc_transpose_i32_ex", _lib.ptr(tp), Bl - e, n, n, _lib.ptr(nbe), Bl,
+                  _lib.ptr(order), h)
+        _lib.call("rfxc_transpose_i32_ex", _lib.ptr(nbe), n, Bl - e, Bl, _lib.ptr(tm[e]), n, None, h)
+        for c0, c1, _ev in rest:
+            mark(c0, c1)
     return nb, tm, done
