@@ -121,7 +121,7 @@ __global__ void pack_kernel(const int8_t* __restrict__ status,
 #define RFXC_TRAV_G 8
 #endif
 #ifndef RFXC_TRAV_ILP
-#define RFXC_TRAV_ILP 2
+#define RFXC_TRAV_ILP 1
 #endif
 constexpr int TRAV_T = 128;             // samples per CTA (one X row each in shared memory)
 constexpr int TRAV_G = RFXC_TRAV_G;     // tree groups per CTA: TRAV_T * TRAV_G threads share the tile
