@@ -123,7 +123,10 @@ __global__ void pack_kernel(const int8_t* __restrict__ status,
 #ifndef RFXC_TRAV_ILP
 #define RFXC_TRAV_ILP 1
 #endif
-constexpr int TRAV_T = 128;             // samples per CTA (one X row each in shared memory)
+#ifndef RFXC_TRAV_T
+#define RFXC_TRAV_T 128
+#endif
+constexpr int TRAV_T = RFXC_TRAV_T;     // samples per CTA (one X row each in shared memory)
 constexpr int TRAV_G = RFXC_TRAV_G;     // tree groups per CTA: TRAV_T * TRAV_G threads share the tile
 constexpr int TRAV_ILP = RFXC_TRAV_ILP; // independent tree chains per thread
 
