@@ -1477,7 +1477,7 @@ extern "C" int rfxc_sketch_pass(const uint32_t* d_perm, const int64_t* d_seg,
     A.s_rows = s_rows;
     A.item = item;
     {   // phase B: all items in one wave of resident warps (4 CTAs x 8 warps per SM)
-        const int64_t warps = (int64_t)sm_count() * 4 * 8;
+        const int64_t warps = (int64_t)sm_count() * SKP_MINB_B * 8;
         A.spw = (int)std::min<int64_t>(SKP_SAMPLES, std::max<int64_t>(1, (n + warps - 1) / warps));
     }
     A.ipb = skp_items_per_batch(n, T, item);
