@@ -738,6 +738,9 @@ constexpr int SKP_UA = 4;
 #ifndef SKP_BRANCHLESS_A
 #define SKP_BRANCHLESS_A 1
 #endif
+#ifndef SKP_JOIN_SHFL
+#define SKP_JOIN_SHFL 1
+#endif
 #ifndef SKP_BL_UNROLL
 #define SKP_BL_UNROLL 2
 #endif
@@ -927,14 +930,22 @@ __device__ void skp_phase_a(const SkpArgs& A, int e, int64_t it, uint32_t* pbuf,
                 }
             }
         }
-        tsm[lane] = acc;
+        if (!SKP_JOIN_SHFL) tsm[lane] = acc;
         __syncwarp();
         // join the slots' cut segments in position order (uniform over the warp)
 #pragma unroll
         for (int j = 0; j < SKP_RMAX; j++) {
             if (j >= R || s0 + j >= nsub) break;
             const int src = j * k4 + c4;
-            const float4 tj = tsm[src];
+            float4 tj;
+            if (SKP_JOIN_SHFL) {  // slot j's tail straight from its lanes' registers
+                tj.x = __shfl_sync(0xffffffffu, acc.x, src);
+                tj.y = __shfl_sync(0xffffffffu, acc.y, src);
+                tj.z = __shfl_sync(0xffffffffu, acc.z, src);
+                tj.w = __shfl_sync(0xffffffffu, acc.w, src);
+            } else {
+                tj = tsm[src];
+            }
             const int curj = __shfl_sync(0xffffffffu, cur, j * k4);
             const unsigned fj = (s0 == 0 && j == 0) ? (fl[j] & ~1u) : fl[j];
             const bool starts = (fl[j] & 1u) != 0;
