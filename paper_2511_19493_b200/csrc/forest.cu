@@ -304,24 +304,36 @@ traverse_kernel(const void* __restrict__ nodes_v, const int64_t* __restrict__ no
     }
 }
 
+#ifndef TRP_TPB
+#define TRP_TPB 4
+#endif
 // out[map(c) * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols
 // (map = identity when col_map is null): 32 x 32 tiles through shared memory
 __global__ void transpose_i32_kernel(const int32_t* __restrict__ in, int64_t rows,
                                      int64_t cols, int64_t ld_in, int32_t* __restrict__ out,
                                      int64_t ld_out, const int32_t* __restrict__ col_map)
 {
-    __shared__ int32_t tile[32][33];
-    const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
-    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-        int64_t r = r0 + k, c = c0 + threadIdx.x;
-        if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * ld_in + c];
+    __shared__ int32_t tile[TRP_TPB][32][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32;
+    // TRP_TPB 32 x 32 tiles stacked along the rows per block, so every output
+    // row gets a 32 * TRP_TPB * 4-byte contiguous segment
+#pragma unroll
+    for (int q = 0; q < TRP_TPB; q++) {
+        const int64_t r0 = ((int64_t)blockIdx.y * TRP_TPB + q) * 32;
+        for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+            int64_t r = r0 + k, c = c0 + threadIdx.x;
+            if (r < rows && c < cols) tile[q][k][threadIdx.x] = in[r * ld_in + c];
+        }
     }
     __syncthreads();
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-        int64_t c = c0 + k, r = r0 + threadIdx.x;
-        if (r < rows && c < cols) {
-            const int64_t oc = col_map ? (int64_t)__ldg(col_map + c) : c;
-            out[oc * ld_out + r] = tile[threadIdx.x][k];
+        const int64_t c = c0 + k;
+        if (c >= cols) continue;
+        const int64_t oc = col_map ? (int64_t)__ldg(col_map + c) : c;
+#pragma unroll
+        for (int q = 0; q < TRP_TPB; q++) {
+            const int64_t r = ((int64_t)blockIdx.y * TRP_TPB + q) * 32 + threadIdx.x;
+            if (r < rows) out[oc * ld_out + r] = tile[q][threadIdx.x][k];
         }
     }
 }
@@ -546,7 +558,7 @@ extern "C" int rfxc_transpose_i32_ex(const int32_t* d_in, int64_t rows, int64_t 
     if (rows < 0 || cols < 0 || ld_in < cols || ld_out < rows)
         return fail(RFXC_EDATA, "transpose: bad shape");
     if (rows == 0 || cols == 0) return RFXC_OK;
-    dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+    dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32 * TRP_TPB));
     transpose_i32_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(d_in, rows, cols, ld_in, d_out, ld_out,
                                                                        d_col_map);
     return check_launch("transpose_i32");
