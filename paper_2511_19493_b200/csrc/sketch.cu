@@ -30,7 +30,10 @@ namespace cg = cooperative_groups;
 namespace rfxc {
 
 // --------------------------------------------------------------- normals
-constexpr int NORMAL_PAIRS_PER_THREAD = 64;
+#ifndef RFXC_NORMAL_PAIRS
+#define RFXC_NORMAL_PAIRS 16
+#endif
+constexpr int NORMAL_PAIRS_PER_THREAD = RFXC_NORMAL_PAIRS;
 
 __global__ void normals_kernel(uint64_t st0, uint64_t inc, int64_t count, double* __restrict__ out)
 {
