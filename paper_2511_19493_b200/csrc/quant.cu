@@ -83,14 +83,16 @@ colmax_kernel(const double* __restrict__ F, int64_t n, int r, int64_t rows_per_p
     }
 }
 
+// a warp per column (max is order-free: the same value as a sequential scan)
 __global__ void colmax_final_kernel(const double* __restrict__ parts, int nparts, int r,
                                      double* __restrict__ scales)
 {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (c >= r) return;
     double m = 0.0;
-    for (int q = 0; q < nparts; q++) m = fmax(m, parts[(int64_t)q * r + c]);
-    scales[c] = m / 127.0;  // quantize.py:95-96
+    for (int q = lane; q < nparts; q += 32) m = fmax(m, __ldg(parts + (int64_t)q * r + c));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) scales[c] = m / 127.0;  // quantize.py:95-96
 }
 
 __global__ void quant_i8_kernel(const double* __restrict__ F, int64_t total, int r,
@@ -231,7 +233,15 @@ pmax_kernel(const double* __restrict__ dq, int64_t n, int r, int64_t rows_per_pa
         const int64_t r0 = blockIdx.x * rows_per_part, r1 = min(n, r0 + rows_per_part);
         for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
             double s = 0.0;
-            for (int c = 0; c < r; c++) s += dq[i * r + c] * dq[i * r + c];
+            if (r == 32) {  // all the row's loads in flight first, then the sum in column order
+                double x[32];
+#pragma unroll
+                for (int c = 0; c < 32; c++) x[c] = __ldg(dq + i * 32 + c);
+#pragma unroll
+                for (int c = 0; c < 32; c++) s += x[c] * x[c];
+            } else {
+                for (int c = 0; c < r; c++) s += dq[i * r + c] * dq[i * r + c];
+            }
             m = fmax(m, s);
         }
     } else {
@@ -240,7 +250,18 @@ pmax_kernel(const double* __restrict__ dq, int64_t n, int r, int64_t rows_per_pa
             const int64_t i = pairs[2 * t], j = pairs[2 * t + 1];
             if (i == j) continue;
             double s = 0.0;
-            for (int c = 0; c < r; c++) s += dq[i * r + c] * dq[j * r + c];
+            if (r == 32) {  // both rows' loads in flight first, then the sum in column order
+                double a[32], b[32];
+#pragma unroll
+                for (int c = 0; c < 32; c++) {
+                    a[c] = __ldg(dq + i * 32 + c);
+                    b[c] = __ldg(dq + j * 32 + c);
+                }
+#pragma unroll
+                for (int c = 0; c < 32; c++) s += a[c] * b[c];
+            } else {
+                for (int c = 0; c < r; c++) s += dq[i * r + c] * dq[j * r + c];
+            }
             m = fmax(m, s);
         }
     }
@@ -259,10 +280,10 @@ __global__ void __launch_bounds__(256) pmax_draws_kernel(uint64_t s0, uint64_t s
 
 __global__ void max_final_kernel(const double* __restrict__ parts, int np, double* out)
 {
-    if (threadIdx.x != 0) return;
-    double m = parts[0];
-    for (int q = 1; q < np; q++) m = fmax(m, parts[q]);
-    *out = m;
+    double m = -INFINITY;  // one warp; max is order-free
+    for (int q = threadIdx.x; q < np; q += 32) m = fmax(m, __ldg(parts + q));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) *out = m;
 }
 
 }  // namespace rfxc
@@ -307,8 +328,8 @@ extern "C" int rfxc_factor_quantize(const double* d_Q, int64_t n, int32_t k, con
     const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 16);
     switch (mode) {
     case RFXC_Q_I8:
-        colmax_final_kernel<<<(unsigned)ceil_div(r, 128), 128, 0, st>>>(d_colmax_parts, parts, r,
-                                                                        d_scales);
+        colmax_final_kernel<<<(unsigned)ceil_div((int64_t)r * 32, 128), 128, 0, st>>>(d_colmax_parts, parts,
+                                                                                   r, d_scales);
         quant_i8_kernel<<<grid, 256, 0, st>>>(d_factor, total, r, d_scales,
                                               reinterpret_cast<int8_t*>(d_data));
         break;
