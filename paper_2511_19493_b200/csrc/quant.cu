@@ -100,7 +100,7 @@ __global__ void quant_i8_kernel(const double* __restrict__ F, int64_t total, int
 {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const double s = scales[e % r];
+        const double s = scales[total < (int64_t(1) << 32) ? (int)((uint32_t)e % (uint32_t)r) : (int)(e % r)];
         const double safe = s > 0.0 ? s : 1.0;
         double q = rint(F[e] / safe);
         q = fmin(127.0, fmax(-127.0, q));
@@ -157,7 +157,8 @@ __global__ void dequant_kernel(const void* __restrict__ data, const double* __re
          e += (int64_t)gridDim.x * blockDim.x) {
         double v;
         if (mode == RFXC_Q_I8) {
-            v = (double)reinterpret_cast<const int8_t*>(data)[e] * scales[e % r];
+            v = (double)reinterpret_cast<const int8_t*>(data)[e] *
+                scales[total < (int64_t(1) << 32) ? (int)((uint32_t)e % (uint32_t)r) : (int)(e % r)];
         } else if (mode == RFXC_Q_F32) {
             v = (double)reinterpret_cast<const float*>(data)[e];
         } else if (mode == RFXC_Q_F16) {

@@ -61,8 +61,15 @@ __global__ void pack_f32_kernel(const double* __restrict__ in, int64_t n, int k,
     const int64_t total = n * ld;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e / ld;
-        const int c = (int)(e % ld);
+        int64_t i;
+        int c;
+        if (total < (int64_t(1) << 32)) {  // 32-bit index math
+            i = (int64_t)((uint32_t)e / (uint32_t)ld);
+            c = (int)((uint32_t)e - (uint32_t)i * (uint32_t)ld);
+        } else {
+            i = e / ld;
+            c = (int)(e % ld);
+        }
         out[e] = c < k ? (float)in[i * k + c] : 0.0f;
     }
 }
