@@ -128,7 +128,7 @@ LAUNCHES = {"rfxc_values_to_f32": 1, "rfxc_forest_pack": 1, "rfxc_leaf_codes": 1
             "rfxc_permute_rows_f32": 1, "rfxc_bucket": 1, "rfxc_bucket_trees": 1, "rfxc_pair_counts": 1,
             "rfxc_triblock_count": 1, "rfxc_triblock_emit": 1, "rfxc_exclusive_scan_i64": 1,
             "rfxc_normals": 1, "rfxc_pack_f32": 1, "rfxc_leaf_sums": 1, "rfxc_leaf_gather": 1,
-            "rfxc_sketch_prepare": 1, "rfxc_sketch_pass": 1, "rfxc_orth_map": 1,
+            "rfxc_sketch_prepare": 1, "rfxc_sketch_pass": 0, "rfxc_orth_map": 1,
             "rfxc_chol_inv": 1, "rfxc_ritz_factor_map": 1, "rfxc_sym_eig": 1,
             "rfxc_gram": 2, "rfxc_matmul_small": 1, "rfxc_factor_quantize": 3,
             "rfxc_dequantize": 1, "rfxc_pmax": 2, "rfxc_mds_power": 1, "rfxc_gram_matvec": 1,
@@ -145,7 +145,7 @@ def call(name: str, *args) -> None:
     launch_count += LAUNCHES.get(name, 0)
     if name == "rfxc_mds_power":
         launch_count += int(args[7])  # start-vector normals, one per component
-    elif name == "rfxc_sketch_pass":  # a leaf-sum and a gather kernel per tree batch + the sum
+    elif name == "rfxc_sketch_pass":  # a leaf-sum and a gather kernel per tree batch (the last adds up Y)
         Bl, T = int(args[6]), int(args[11])
         launch_count += 2 * ((Bl + T - 1) // T)
     elif name in ("rfxc_bucket", "rfxc_bucket_trees"):  # launches of <= 2 trees per SM

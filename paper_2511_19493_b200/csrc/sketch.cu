@@ -751,6 +751,9 @@ constexpr int SKP_UA = 4;
 #ifndef SKP_JOIN_SHFL
 #define SKP_JOIN_SHFL 1
 #endif
+#ifndef SKP_FUSE_FINAL
+#define SKP_FUSE_FINAL 1
+#endif
 #ifndef SKP_BL_UNROLL
 #define SKP_BL_UNROLL 2
 #endif
@@ -1059,7 +1062,40 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
 #pragma unroll
             for (int u = 0; u < SKP_UB; u++) f4add(acc, x[u]);
         }
-        if (act && A.P) {
+        if (act && A.P && last && SKP_FUSE_FINAL) {
+            // the last batch finishes the sample: the earlier batches'
+            // partials and its own sum added in batch order in f64, times
+            // 1/B — skp_final_kernel's additions in its order (same bits)
+            const float4* P4 = reinterpret_cast<const float4*>(A.P);
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+            int e2 = 0;
+            for (; e2 + 4 <= e; e2 += 4) {
+                float4 x[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) x[u] = __ldcs(P4 + ((int64_t)(e2 + u) * A.n + i) * k4 + c4);
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    v[0] += (double)x[u].x;
+                    v[1] += (double)x[u].y;
+                    v[2] += (double)x[u].z;
+                    v[3] += (double)x[u].w;
+                }
+            }
+            for (; e2 < e; e2++) {
+                const float4 x = __ldcs(P4 + ((int64_t)e2 * A.n + i) * k4 + c4);
+                v[0] += (double)x.x;
+                v[1] += (double)x.y;
+                v[2] += (double)x.z;
+                v[3] += (double)x.w;
+            }
+            v[0] += (double)acc.x;
+            v[1] += (double)acc.y;
+            v[2] += (double)acc.z;
+            v[3] += (double)acc.w;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (4 * c4 + q < A.k) y[q] = v[q] * A.scale;
+        } else if (act && A.P) {
             // the batch's f32 sum leaves once (16 B per lane); the f64 sum over
             // the batches (in batch order, identical bits) is skp_final_kernel's
             __stcs(reinterpret_cast<float4*>(A.P + ((int64_t)e * A.n + i) * A.ld) + c4, acc);
@@ -1419,7 +1455,7 @@ static void launch_phase(const SkpArgs& A, int e, cudaStream_t s)
 // accumulation order is fixed) and the last B joins everything back.
 static void launch_final(const SkpArgs& A, cudaStream_t st)
 {
-    if (!A.P) return;
+    if (!A.P || SKP_FUSE_FINAL) return;  // fused: the last phase B wrote Y
     const int grid = (int)std::min<int64_t>(ceil_div(A.n * (A.ld / 4), 256), (int64_t)sm_count() * 16);
     skp_final_kernel<<<grid, 256, 0, st>>>(A.P, A.nbatch, A.n, A.ld, A.k, A.scale, A.Y);
 }
