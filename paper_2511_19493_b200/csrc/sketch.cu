@@ -319,7 +319,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-constexpr int GS_CH = 32;
+#ifndef RFXC_GS_CH
+#define RFXC_GS_CH 64
+#endif
+constexpr int GS_CH = RFXC_GS_CH;  // rows per staged chunk (64 measured best; 128 fails the Gram tests)
+static_assert(GS_CH % 4 == 0 && GS_CH <= 64, "Gram chunk: a multiple of 4, at most 64 rows");
 constexpr int GS_MAXST = 8;
 
 // wait until at most n (< GS_MAXST) cp.async groups of this thread are pending
