@@ -319,11 +319,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-#ifndef RFXC_GS_CH
-#define RFXC_GS_CH 64
-#endif
-constexpr int GS_CH = RFXC_GS_CH;  // rows per staged chunk (64 measured best; 128 fails the Gram tests)
-static_assert(GS_CH % 4 == 0 && GS_CH <= 64, "Gram chunk: a multiple of 4, at most 64 rows");
+// rows per staged chunk: 64 (measured best) when two stages fit the shared
+// memory, else 32 (wide non-symmetric Grams)
+constexpr int GS_CH_BIG = 64, GS_CH_SMALL = 32;
 constexpr int GS_MAXST = 8;
 
 // wait until at most n (< GS_MAXST) cp.async groups of this thread are pending
@@ -352,7 +350,7 @@ __host__ __device__ inline int gs_ld(int cols) { return cols + ((4 - cols % 16) 
 
 constexpr int GS_THREADS = 512;
 
-template <int MT>
+template <int MT, int GS_CH>
 __global__ void __launch_bounds__(GS_THREADS, 1)
 gram_stage_kernel(const double* __restrict__ A, const double* __restrict__ Bm, int64_t n, int ka,
                   int kb, int sym, int64_t rpp, int nst, double* __restrict__ parts)
@@ -454,6 +452,24 @@ gram_stage_kernel(const double* __restrict__ A, const double* __restrict__ Bm, i
     }
 }
 
+template <int MT, int GS_CH>
+static void gram_stage_go(const double* d_A, const double* d_B, int64_t n, int ka, int kb, int sym,
+                          int parts, int64_t rpp, double* d_partials, cudaStream_t st)
+{
+    const int TA = (ka + 7) / 8, TB = (kb + 7) / 8;
+    const size_t per = (size_t)GS_CH * (gs_ld(8 * TA) + (sym ? 0 : gs_ld(8 * TB))) * 8;
+    const int nst = (int)std::max<size_t>(2, std::min<size_t>(GS_MAXST, (size_t)(200 * 1024) / per));
+    const size_t smem = per * nst;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gram_stage_kernel<MT, GS_CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+    }
+    gram_stage_kernel<MT, GS_CH><<<parts, GS_THREADS, smem, st>>>(d_A, d_B, n, ka, kb, sym, rpp, nst,
+                                                                   d_partials);
+}
+
 template <int MT>
 static int launch_gram_stage(const double* d_A, const double* d_B, int64_t n, int ka, int kb,
                              double* d_partials, double* d_C, cudaStream_t st)
@@ -462,16 +478,11 @@ static int launch_gram_stage(const double* d_A, const double* d_B, int64_t n, in
     const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 64), sm_count()));
     const int64_t rpp = ceil_div(n, parts);
     const int TA = (ka + 7) / 8, TB = (kb + 7) / 8;
-    const size_t per = (size_t)GS_CH * (gs_ld(8 * TA) + (sym ? 0 : gs_ld(8 * TB))) * 8;
-    const int nst = (int)std::max<size_t>(2, std::min<size_t>(GS_MAXST, (size_t)(200 * 1024) / per));
-    const size_t smem = per * nst;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(gram_stage_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        attr = true;
-    }
-    gram_stage_kernel<MT><<<parts, GS_THREADS, smem, st>>>(d_A, d_B, n, ka, kb, sym, rpp, nst, d_partials);
+    const size_t per_big = (size_t)GS_CH_BIG * (gs_ld(8 * TA) + (sym ? 0 : gs_ld(8 * TB))) * 8;
+    if (2 * per_big <= (size_t)200 * 1024)
+        gram_stage_go<MT, GS_CH_BIG>(d_A, d_B, n, ka, kb, sym, parts, rpp, d_partials, st);
+    else
+        gram_stage_go<MT, GS_CH_SMALL>(d_A, d_B, n, ka, kb, sym, parts, rpp, d_partials, st);
     int rc = check_launch("gram_stage");
     if (rc) return rc;
     gram_final_kernel<<<(unsigned)ceil_div((int64_t)ka * kb * 32, 256), 256, 0, st>>>(

@@ -118,7 +118,8 @@ def test_ritz_factor_map_matches_host():
 @pytest.mark.parametrize("n,ka,kb,same", [(1, 3, 3, True), (5, 8, 8, True), (178, 24, 24, True),
                                           (178, 24, 24, False), (1000, 40, 16, False),
                                           (100_003, 40, 40, True), (4099, 108, 108, True),
-                                          (777, 130, 24, False)])
+                                          (777, 130, 24, False), (5003, 120, 120, False),
+                                          (5003, 128, 96, False), (70_001, 40, 40, False)])
 def test_gram_matches_numpy(built, n, ka, kb, same):
     """rfxc_gram (A^T B, f64, fixed-order partial sums) against numpy."""
     import torch
