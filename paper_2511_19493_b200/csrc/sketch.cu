@@ -1112,7 +1112,8 @@ __device__ void skp_phase_b(const SkpArgs& A, int e, int64_t it, uint32_t* rbuf,
                 if (4 * c4 + q < A.k) y[q] = v[q] * A.scale;
         } else if (act && A.P) {
             // the batch's f32 sum leaves once (16 B per lane); the f64 sum over
-            // the batches (in batch order, identical bits) is skp_final_kernel's
+            // the batches (in batch order) is the last batch's (above), or
+            // skp_final_kernel's when SKP_FUSE_FINAL is off
             __stcs(reinterpret_cast<float4*>(A.P + ((int64_t)e * A.n + i) * A.ld) + c4, acc);
         } else if (act) {
             const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
